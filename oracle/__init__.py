@@ -1,0 +1,229 @@
+"""ctypes binding of the CPU oracle (oracle/shiftk_oracle.c) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` legs
+may import this package.  The product package (paper_2001_08707_b200) never imports it, and
+the oracle never imports the product package; both take their inputs from ``synth``.
+
+Parity status of each oracle function:
+  or_heisenberg_apply  pinned: Table 3 eigenvalues, ferromagnet, one-magnon waves
+  or_csr_*_apply       pinned: scipy.sparse product on the same CSR arrays
+  or_update (COCG)     pinned: dense solves, Lanczos continued fraction, pi = chi ratio,
+                       collinearity, b^dagger r_n = 0, exact termination, sum rule
+  or_update (BiCG)     pinned: dense solves, bi-orthogonality, BiCG == COCG on real H
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "shiftk_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+COCG, BICG = 0, 1
+ITERATING, CONVERGED, MAXITER, BREAKDOWN = 0, 1, 2, 3
+FLAG_REVERSE, FLAG_NO_SWITCH = 1, 2
+STATUS_NAMES = {0: "iterating", 1: "converged", 2: "maxiter", 3: "breakdown"}
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc (no fast-math, no BLAS)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", "-o", _LIB_PATH, _SRC, "-lm"])
+    return _LIB_PATH
+
+
+_lib = None
+_c128p = ctypes.c_void_p
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        L = _lib
+        L.or_create.restype = ctypes.c_void_p
+        L.or_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _c128p, _c128p,
+                                ctypes.c_int64, _c128p, ctypes.c_int, ctypes.c_double,
+                                ctypes.c_int64, ctypes.c_int]
+        L.or_destroy.argtypes = [ctypes.c_void_p]
+        L.or_update.restype = ctypes.c_int
+        L.or_update.argtypes = [ctypes.c_void_p, _c128p, _c128p]
+        L.or_heisenberg_apply.argtypes = [ctypes.c_int, ctypes.c_double, _c128p, _c128p]
+        L.or_csr_real_apply.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, _c128p, _c128p]
+        L.or_csr_cplx_apply.argtypes = L.or_csr_real_apply.argtypes
+        for name, rt in [("or_status", ctypes.c_int), ("or_iterations", ctypes.c_int64),
+                         ("or_switches", ctypes.c_int64), ("or_spmv_count", ctypes.c_int64),
+                         ("or_seed_index", ctypes.c_int64), ("or_r", ctypes.c_void_p),
+                         ("or_r_old", ctypes.c_void_p), ("or_t", ctypes.c_void_p),
+                         ("or_pi", ctypes.c_void_p), ("or_pi_old", ctypes.c_void_p),
+                         ("or_res", ctypes.c_void_p), ("or_active", ctypes.c_void_p),
+                         ("or_retired_at", ctypes.c_void_p), ("or_y", ctypes.c_void_p)]:
+            getattr(L, name).restype = rt
+            getattr(L, name).argtypes = [ctypes.c_void_p]
+        L.or_x.restype = ctypes.c_void_p
+        L.or_x.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.or_scalars.argtypes = [ctypes.c_void_p, _c128p]
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _view(addr: int, n: int, dtype) -> np.ndarray:
+    """Copy n elements of dtype from a C pointer."""
+    dt = np.dtype(dtype)
+    buf = (ctypes.c_char * (n * dt.itemsize)).from_address(addr)
+    return np.frombuffer(buf, dtype=dt, count=n).copy()
+
+
+# ------------------------------------------------------------------------------- operators
+
+def heisenberg_apply(L: int, J: float, r: np.ndarray) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.complex128)
+    q = np.empty_like(r)
+    lib().or_heisenberg_apply(L, J, _ptr(r), _ptr(q))
+    return q
+
+
+def csr_apply(op: dict, r: np.ndarray) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.complex128)
+    q = np.empty_like(r)
+    M = op["row_ptr"].shape[0] - 1
+    fn = lib().or_csr_real_apply if op["kind"] == "csr_real" else lib().or_csr_cplx_apply
+    fn(M, _ptr(op["row_ptr"]), _ptr(op["col"]), _ptr(op["val"]), _ptr(r), _ptr(q))
+    return q
+
+
+def apply_op(op: dict, r: np.ndarray) -> np.ndarray:
+    """q = H r with the oracle's own operator code."""
+    if op["kind"] == "heisenberg":
+        return heisenberg_apply(op["L"], op["J"], r)
+    return csr_apply(op, r)
+
+
+# ------------------------------------------------------------------------------- solver
+
+class Oracle:
+    """Reverse-communication shifted COCG/BiCG state machine (init/update/get/finalize,
+    P:L517-523, Alg. 1)."""
+
+    def __init__(self, method: str, b: np.ndarray, z: np.ndarray, *, left: Optional[np.ndarray] = None,
+                 full_x: bool = False, tol: float = 1e-10, itermax: int = 10000, flags: int = 0):
+        self.method = COCG if method == "cocg" else BICG
+        self.b = np.ascontiguousarray(b, dtype=np.complex128)
+        self.z = np.ascontiguousarray(z, dtype=np.complex128)
+        self.M, self.nz = self.b.shape[0], self.z.shape[0]
+        self.left = None if left is None else np.ascontiguousarray(left, dtype=np.complex128)
+        self.nleft = 1 if left is None else self.left.shape[0]
+        self.full_x = bool(full_x)
+        self._h = lib().or_create(self.method, self.M, self.nz, _ptr(self.z), _ptr(self.b),
+                                  self.nleft, 0 if self.left is None else _ptr(self.left),
+                                  int(self.full_x), float(tol), int(itermax), int(flags))
+        if not self._h:
+            raise ValueError("oracle init rejected its arguments")
+
+    def close(self):
+        if self._h:
+            lib().or_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # reverse communication -----------------------------------------------------------
+    def r(self) -> np.ndarray:
+        return _view(lib().or_r(self._h), self.M, np.complex128)
+
+    def r_old(self) -> np.ndarray:
+        return _view(lib().or_r_old(self._h), self.M, np.complex128)
+
+    def t(self) -> np.ndarray:
+        return _view(lib().or_t(self._h), self.M, np.complex128)
+
+    def update(self, q: np.ndarray, qt: Optional[np.ndarray] = None) -> int:
+        q = np.ascontiguousarray(q, dtype=np.complex128)
+        qt_p = 0
+        if self.method == BICG:
+            qt = np.ascontiguousarray(qt, dtype=np.complex128)
+            qt_p = _ptr(qt)
+        return lib().or_update(self._h, _ptr(q), qt_p)
+
+    def step(self, op: dict) -> int:
+        """One iteration with the oracle's own operator: q = H r (and H t for BiCG), update."""
+        q = apply_op(op, self.r())
+        qt = apply_op(op, self.t()) if self.method == BICG else None
+        return self.update(q, qt)
+
+    def run(self, op: dict, max_iters: int) -> int:
+        st = self.status
+        for _ in range(max_iters):
+            st = self.step(op)
+            if st != ITERATING:
+                break
+        return st
+
+    # getters -------------------------------------------------------------------------
+    @property
+    def status(self) -> int:
+        return lib().or_status(self._h)
+
+    @property
+    def iterations(self) -> int:
+        return lib().or_iterations(self._h)
+
+    @property
+    def switches(self) -> int:
+        return lib().or_switches(self._h)
+
+    @property
+    def spmv_count(self) -> int:
+        return lib().or_spmv_count(self._h)
+
+    @property
+    def seed_index(self) -> int:
+        return lib().or_seed_index(self._h)
+
+    def residuals(self) -> np.ndarray:
+        return _view(lib().or_res(self._h), self.nz, np.float64)
+
+    def active(self) -> np.ndarray:
+        return _view(lib().or_active(self._h), self.nz, np.uint8).astype(bool)
+
+    def retired_at(self) -> np.ndarray:
+        return _view(lib().or_retired_at(self._h), self.nz, np.int64)
+
+    def pi(self) -> np.ndarray:
+        return _view(lib().or_pi(self._h), self.nz, np.complex128)
+
+    def pi_old(self) -> np.ndarray:
+        return _view(lib().or_pi_old(self._h), self.nz, np.complex128)
+
+    def projections(self) -> np.ndarray:
+        """y[k, l] = a_l^dagger x^(k) from the projected recurrences."""
+        return _view(lib().or_y(self._h), self.nz * self.nleft, np.complex128).reshape(self.nz, self.nleft)
+
+    def solution(self, k: int) -> np.ndarray:
+        if not self.full_x:
+            raise ValueError("full x not stored")
+        return _view(lib().or_x(self._h, k), self.M, np.complex128)
+
+    def scalars(self) -> dict:
+        out = np.zeros(6, dtype=np.complex128)
+        lib().or_scalars(self._h, _ptr(out))
+        return dict(alpha=out[0], beta=out[1], rho=out[2], w=out[3], z_seed=out[4], alpha_prev=out[5])
+
+
+def solve(problem, max_iters: Optional[int] = None, flags: int = 0) -> Oracle:
+    """Run the oracle on a synth.Problem until convergence / max_iters."""
+    o = Oracle(problem.method, problem.b, problem.z, left=problem.left, full_x=problem.full_x,
+               tol=problem.tol, itermax=problem.itermax, flags=flags)
+    o.run(problem.op, problem.itermax if max_iters is None else max_iters)
+    return o

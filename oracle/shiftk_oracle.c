@@ -1,0 +1,355 @@
+/*
+ * shiftk_oracle.c — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the shifted COCG / shifted BiCG
+ * iteration of the Komega paper (arxiv 2001.08707; PAPER.md = /root/reference/PAPER.md,
+ * cited P:Lnnn) and of the two operators on the hot path.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or helper with the CUDA path (paper_2001_08707_b200/csrc).
+ *
+ * Arithmetic: IEEE fp64, C99 `double complex`, every reduction a fixed-order loop over
+ * i = 0..M-1 (or M-1..0 with OR_FLAG_REVERSE, used only to measure the self-divergence
+ * horizon of SURVEY §8(c.4)).  Single-threaded.
+ *
+ * Algorithm (one call of or_update = one iteration n; step numbers follow SURVEY §8(c.1)):
+ *   inner product  <u,v> = sum u_i v_i (COCG, App. A)  |  sum conj(u_i) v_i (BiCG)
+ *   A = z_s I - H  (EQ-SHIFT-EQ2), so  A r = z_s r - q  with q = H r supplied by the caller
+ *   2  rho_n = <r_n, r_n> | <t_n, r_n>,  w_n = <r_n, q> | <t_n, q>
+ *   3  beta_{n-1} = rho_n / rho_{n-1}  (EQ-REC-BETA P:L262), gamma = beta_{n-1}/alpha_{n-1},
+ *      gamma = 0 at n = 0 ("start with beta_{-1}/alpha_{-1} = 0")
+ *   4  alpha_n = rho_n / (<r, A r> - gamma rho_n),  <r, A r> = z_s rho_n - w_n   (EQ-REC-ALPHA-N2 P:L276)
+ *   5  c_n = alpha_n gamma = alpha_n beta_{n-1} / alpha_{n-1}
+ *   6  per active shift k, sigma = z_k - z_s:
+ *        pi_{n+1} = (1 + c_n + alpha_n sigma) pi_n - c_n pi_{n-1}                  (EQ-SHIFTEDCG-PI P:L317)
+ *        alpha_n^k = (pi_n / pi_{n+1}) alpha_n                                       (EQ-SHIFTEDCG-alpha P:L325)
+ *        beta_{n-1}^k = (pi_{n-1} / pi_n)^2 beta_{n-1}                              (EQ-SHIFTEDCG-beta P:L326)
+ *   7  full:  p_n^k = r_n / pi_n^k + beta_{n-1}^k p_{n-1}^k ; x_{n+1}^k = x_n^k + alpha_n^k p_n^k
+ *                                                                                    (EQ-SHIFTEDCG-x/p P:L327-328)
+ *      proj:  g_n = P r_n (g_l = a_l^dagger r_n);  u_n^k = g_n / pi_n^k + beta_{n-1}^k u_{n-1}^k ;
+ *             y_{n+1}^k = y_n^k + alpha_n^k u_n^k      (EQ-SHIFTEDCG-y/u P:L372-376 with the index
+ *             of P:L373 read as pi_{n+1} / r_{n+1} for u_{n+1}, i.e. as EQ-SHIFTEDCG-p; R1)
+ *   8  r_{n+1} = (1 + c_n) r_n - alpha_n A r_n - c_n r_{n-1}                       (EQ-CG-RN-3REC P:L269)
+ *      BiCG:  t_{n+1} = (1 + c_n^*) t_n - alpha_n^* A^dagger t_n - c_n^* t_{n-1},
+ *             A^dagger t = z_s^* t - H t  (H Hermitian)                               (App. B)
+ *   9  pi_{n-1} <- pi_n, pi_n <- pi_{n+1}; alpha_prev <- alpha_n; rho_prev <- rho_n
+ *  10  nu = ||r_{n+1}||_2 ("2-norm"); res_k = nu / |pi_{n+1}^k| (EQ-COLLINEAR P:L300);
+ *      retire k when res_k < tol (frozen thereafter, R8)
+ *  11  CONVERGED when no shift is active; MAXITER when n+1 = itermax
+ *  12  seed switch ("always ... after an update"): s* = argmin_{k active} |pi_{n+1}^k|,
+ *      lowest index on ties; if s* != s:  f = pi_{n+1}^{s*}, f' = pi_n^{s*};
+ *      r_{n+1} /= f, r_n /= f' (shadow by conj);  active pi_{n+1} /= f, pi_n /= f';
+ *      alpha_prev *= f'/f (EQ-SHIFTEDCG-alpha);  rho_prev /= f'^2;  z_s = z_{s*}   (R9)
+ *
+ * Breakdown (R12): |rho_n| < 1e-300 or |alpha denominator| < 1e-300 -> OR_BREAKDOWN.
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef double complex cplx;
+
+enum { OR_COCG = 0, OR_BICG = 1 };
+enum { OR_ITERATING = 0, OR_CONVERGED = 1, OR_MAXITER = 2, OR_BREAKDOWN = 3 };
+enum { OR_FLAG_REVERSE = 1, OR_FLAG_NO_SWITCH = 2 };
+
+typedef struct {
+    int method, full, flags;
+    int64_t M, nz, nleft, itermax;
+    double tol;
+    cplx *b, *left;            /* left: [nleft][M] (copy of b when a = b) */
+    cplx *r, *r_old, *t, *t_old, *tmp;
+    cplx *z, zs;
+    int64_t s;
+    cplx *pi, *pi_old, *pi_new;
+    unsigned char *active;
+    double *res;
+    int64_t *retired_at;
+    cplx *g, *u, *y;           /* g: [nleft]; u, y: [nz][nleft] */
+    cplx *p, *x;               /* [nz][M] when full */
+    cplx alpha_prev, rho_prev;
+    cplx alpha, beta, rho, w;  /* last iteration's seed scalars (for inspection) */
+    int64_t n, nswitch, nspmv;
+    int status;
+} or_state;
+
+/* ------------------------------------------------------------------ inner products */
+
+static cplx dot_plain(const or_state *st, const cplx *u, const cplx *v) {
+    cplx acc = 0;
+    if (st->flags & OR_FLAG_REVERSE) {
+        for (int64_t i = st->M - 1; i >= 0; --i) acc += u[i] * v[i];
+    } else {
+        for (int64_t i = 0; i < st->M; ++i) acc += u[i] * v[i];
+    }
+    return acc;
+}
+
+static cplx dot_conj(const or_state *st, const cplx *u, const cplx *v) {
+    cplx acc = 0;
+    if (st->flags & OR_FLAG_REVERSE) {
+        for (int64_t i = st->M - 1; i >= 0; --i) acc += conj(u[i]) * v[i];
+    } else {
+        for (int64_t i = 0; i < st->M; ++i) acc += conj(u[i]) * v[i];
+    }
+    return acc;
+}
+
+/* <u, v> of the method: unconjugated for COCG (App. A), conjugated for BiCG (App. B) */
+static cplx dot_method(const or_state *st, const cplx *u, const cplx *v) {
+    return st->method == OR_COCG ? dot_plain(st, u, v) : dot_conj(st, u, v);
+}
+
+/* g_l = a_l^dagger v  (projection P v) */
+static void project(const or_state *st, const cplx *v, cplx *g) {
+    for (int64_t l = 0; l < st->nleft; ++l) g[l] = dot_conj(st, st->left + l * st->M, v);
+}
+
+/* ------------------------------------------------------------------ lifecycle */
+
+static void *xcalloc(size_t n, size_t sz) { return calloc(n ? n : 1, sz); }
+
+void or_destroy(or_state *st);
+
+/* left == NULL  ->  a = b (one left vector equal to b). */
+or_state *or_create(int method, int64_t M, int64_t nz, const cplx *z, const cplx *b,
+                    int64_t nleft, const cplx *left, int full, double tol, int64_t itermax,
+                    int flags) {
+    if (M <= 0 || nz <= 0 || (method != OR_COCG && method != OR_BICG) || tol <= 0 || itermax < 1)
+        return NULL;
+    or_state *st = (or_state *)xcalloc(1, sizeof(or_state));
+    st->method = method; st->M = M; st->nz = nz; st->full = full; st->tol = tol;
+    st->itermax = itermax; st->flags = flags;
+    st->nleft = left ? nleft : 1;
+    st->b = (cplx *)xcalloc(M, sizeof(cplx));
+    st->left = (cplx *)xcalloc(st->nleft * M, sizeof(cplx));
+    st->r = (cplx *)xcalloc(M, sizeof(cplx));
+    st->r_old = (cplx *)xcalloc(M, sizeof(cplx));
+    st->tmp = (cplx *)xcalloc(M, sizeof(cplx));
+    if (method == OR_BICG) {
+        st->t = (cplx *)xcalloc(M, sizeof(cplx));
+        st->t_old = (cplx *)xcalloc(M, sizeof(cplx));
+    }
+    st->z = (cplx *)xcalloc(nz, sizeof(cplx));
+    st->pi = (cplx *)xcalloc(nz, sizeof(cplx));
+    st->pi_old = (cplx *)xcalloc(nz, sizeof(cplx));
+    st->pi_new = (cplx *)xcalloc(nz, sizeof(cplx));
+    st->active = (unsigned char *)xcalloc(nz, 1);
+    st->res = (double *)xcalloc(nz, sizeof(double));
+    st->retired_at = (int64_t *)xcalloc(nz, sizeof(int64_t));
+    st->g = (cplx *)xcalloc(st->nleft, sizeof(cplx));
+    st->u = (cplx *)xcalloc(nz * st->nleft, sizeof(cplx));
+    st->y = (cplx *)xcalloc(nz * st->nleft, sizeof(cplx));
+    if (full) {
+        st->p = (cplx *)xcalloc((size_t)(nz * M), sizeof(cplx));
+        st->x = (cplx *)xcalloc((size_t)(nz * M), sizeof(cplx));
+        if (!st->p || !st->x) { or_destroy(st); return NULL; }
+    }
+    memcpy(st->b, b, M * sizeof(cplx));
+    memcpy(st->z, z, nz * sizeof(cplx));
+    if (left) memcpy(st->left, left, nleft * M * sizeof(cplx));
+    else memcpy(st->left, b, M * sizeof(cplx));
+
+    /* Init: r_0 = b, r_{-1} = 0, t_0 = conj(b) (R3), pi_0 = pi_{-1} = 1,
+       x_0 = 0, y_0 = 0, first seed z[0]. */
+    memcpy(st->r, b, M * sizeof(cplx));
+    if (method == OR_BICG)
+        for (int64_t i = 0; i < M; ++i) st->t[i] = conj(b[i]);
+    double nb = sqrt(creal(dot_conj(st, b, b)));
+    for (int64_t k = 0; k < nz; ++k) {
+        st->pi[k] = 1; st->pi_old[k] = 1; st->active[k] = 1; st->res[k] = nb;
+        st->retired_at[k] = -1;
+    }
+    st->s = 0; st->zs = z[0];
+    st->n = 0; st->status = OR_ITERATING;
+    return st;
+}
+
+void or_destroy(or_state *st) {
+    if (!st) return;
+    free(st->b); free(st->left); free(st->r); free(st->r_old); free(st->tmp);
+    free(st->t); free(st->t_old); free(st->z); free(st->pi); free(st->pi_old); free(st->pi_new);
+    free(st->active); free(st->res); free(st->retired_at); free(st->g); free(st->u); free(st->y);
+    free(st->p); free(st->x);
+    free(st);
+}
+
+/* ------------------------------------------------------------------ one iteration */
+
+/* q = H r_n (and qt = H t_n for BiCG), computed by the caller (reverse communication,
+   P:L503-508; Alg. 1). */
+int or_update(or_state *st, const cplx *q, const cplx *qt) {
+    if (st->status != OR_ITERATING) return st->status;
+    const int64_t M = st->M, nz = st->nz, nl = st->nleft, n = st->n;
+    const int bicg = st->method == OR_BICG;
+    const cplx *tv = bicg ? st->t : st->r;    /* left operand of the method's inner product */
+    st->nspmv += bicg ? 2 : 1;
+
+    /* 2 */
+    cplx rho = dot_method(st, tv, st->r);
+    cplx w = dot_method(st, tv, q);
+    /* 3 */
+    cplx beta = 0, gamma = 0;
+    if (n > 0) { beta = rho / st->rho_prev; gamma = beta / st->alpha_prev; }
+    /* 4 */
+    cplx den = st->zs * rho - w - gamma * rho;
+    if (cabs(rho) < 1e-300 || cabs(den) < 1e-300) { st->status = OR_BREAKDOWN; return st->status; }
+    cplx alpha = rho / den;
+    /* 5 */
+    cplx c = alpha * gamma;
+    st->alpha = alpha; st->beta = beta; st->rho = rho; st->w = w;
+
+    /* 6 + 7 */
+    if (nl > 0) project(st, st->r, st->g);
+    for (int64_t k = 0; k < nz; ++k) {
+        if (!st->active[k]) continue;
+        cplx sigma = st->z[k] - st->zs;
+        cplx pin = (1.0 + c + alpha * sigma) * st->pi[k] - c * st->pi_old[k];
+        cplx ak = (st->pi[k] / pin) * alpha;
+        cplx rat = st->pi_old[k] / st->pi[k];
+        cplx bk = (n == 0) ? 0 : rat * rat * beta;
+        st->pi_new[k] = pin;
+        for (int64_t l = 0; l < nl; ++l) {
+            cplx *u = st->u + k * nl + l, *y = st->y + k * nl + l;
+            *u = st->g[l] / st->pi[k] + bk * (*u);
+            *y = *y + ak * (*u);
+        }
+        if (st->full) {
+            cplx *p = st->p + k * M, *x = st->x + k * M;
+            for (int64_t i = 0; i < M; ++i) {
+                p[i] = st->r[i] / st->pi[k] + bk * p[i];
+                x[i] = x[i] + ak * p[i];
+            }
+        }
+    }
+
+    /* 8 */
+    for (int64_t i = 0; i < M; ++i)
+        st->tmp[i] = (1.0 + c) * st->r[i] - alpha * (st->zs * st->r[i] - q[i]) - c * st->r_old[i];
+    { cplx *o = st->r_old; st->r_old = st->r; st->r = st->tmp; st->tmp = o; }
+    if (bicg) {
+        cplx cc = conj(c), ac = conj(alpha), zc = conj(st->zs);
+        for (int64_t i = 0; i < M; ++i)
+            st->tmp[i] = (1.0 + cc) * st->t[i] - ac * (zc * st->t[i] - qt[i]) - cc * st->t_old[i];
+        cplx *o = st->t_old; st->t_old = st->t; st->t = st->tmp; st->tmp = o;
+    }
+
+    /* 9 */
+    for (int64_t k = 0; k < nz; ++k) {
+        if (!st->active[k]) continue;
+        st->pi_old[k] = st->pi[k];
+        st->pi[k] = st->pi_new[k];
+    }
+    st->alpha_prev = alpha;
+    st->rho_prev = rho;
+    st->n = n + 1;
+
+    /* 10 */
+    double nu = sqrt(creal(dot_conj(st, st->r, st->r)));
+    int64_t nact = 0;
+    for (int64_t k = 0; k < nz; ++k) {
+        if (!st->active[k]) continue;
+        st->res[k] = nu / cabs(st->pi[k]);
+        if (st->res[k] < st->tol) { st->active[k] = 0; st->retired_at[k] = n + 1; }
+        else ++nact;
+    }
+    /* 11 */
+    if (nact == 0) { st->status = OR_CONVERGED; return st->status; }
+
+    /* 12 */
+    if (!(st->flags & OR_FLAG_NO_SWITCH)) {
+        int64_t best = -1; double bmin = 0;
+        for (int64_t k = 0; k < nz; ++k) {
+            if (!st->active[k]) continue;
+            double a = cabs(st->pi[k]);
+            if (best < 0 || a < bmin) { best = k; bmin = a; }
+        }
+        if (best != st->s) {
+            cplx f = st->pi[best], fp = st->pi_old[best];
+            for (int64_t i = 0; i < M; ++i) { st->r[i] /= f; st->r_old[i] /= fp; }
+            if (bicg) {
+                cplx fc = conj(f), fpc = conj(fp);
+                for (int64_t i = 0; i < M; ++i) { st->t[i] /= fc; st->t_old[i] /= fpc; }
+            }
+            for (int64_t k = 0; k < nz; ++k) {
+                if (!st->active[k]) continue;
+                st->pi[k] /= f; st->pi_old[k] /= fp;
+            }
+            st->alpha_prev *= fp / f;
+            st->rho_prev /= fp * fp;
+            st->zs = st->z[best];
+            st->s = best;
+            st->nswitch++;
+        }
+    }
+    if (st->n >= st->itermax) st->status = OR_MAXITER;
+    return st->status;
+}
+
+/* ------------------------------------------------------------------ operators */
+
+/* S=1/2 Heisenberg chain H = J sum_{i=0}^{L-1} S_i . S_{i+1}, periodic.  Basis state s
+   is an L-bit integer, bit i = site i, bit value 1 = up (R16).  Per bond (i, i+1):
+   S^z S^z gives +J/4 (aligned) or -J/4 (anti-aligned); (S^+S^- + S^-S^+)/2 flips an
+   anti-aligned pair with amplitude J/2. */
+void or_heisenberg_apply(int L, double J, const cplx *r, cplx *q) {
+    const int64_t M = (int64_t)1 << L;
+    for (int64_t s = 0; s < M; ++s) {
+        cplx acc = 0;
+        for (int i = 0; i < L; ++i) {
+            int j = (i + 1) % L;
+            int bi = (int)((s >> i) & 1), bj = (int)((s >> j) & 1);
+            if (bi == bj) {
+                acc += 0.25 * J * r[s];
+            } else {
+                acc += -0.25 * J * r[s];
+                int64_t s2 = s ^ (((int64_t)1 << i) | ((int64_t)1 << j));
+                acc += 0.5 * J * r[s2];
+            }
+        }
+        q[s] = acc;
+    }
+}
+
+/* q = H r for a CSR matrix with real values (row_ptr int64[M+1], col int32[nnz]). */
+void or_csr_real_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, const double *val,
+                       const cplx *r, cplx *q) {
+    for (int64_t i = 0; i < M; ++i) {
+        cplx acc = 0;
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
+        q[i] = acc;
+    }
+}
+
+/* q = H r for a CSR matrix with complex values. */
+void or_csr_cplx_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, const cplx *val,
+                       const cplx *r, cplx *q) {
+    for (int64_t i = 0; i < M; ++i) {
+        cplx acc = 0;
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
+        q[i] = acc;
+    }
+}
+
+/* ------------------------------------------------------------------ accessors */
+
+int or_status(const or_state *st) { return st->status; }
+int64_t or_iterations(const or_state *st) { return st->n; }
+int64_t or_switches(const or_state *st) { return st->nswitch; }
+int64_t or_spmv_count(const or_state *st) { return st->nspmv; }
+int64_t or_seed_index(const or_state *st) { return st->s; }
+const cplx *or_r(const or_state *st) { return st->r; }
+const cplx *or_r_old(const or_state *st) { return st->r_old; }
+const cplx *or_t(const or_state *st) { return st->t; }
+const cplx *or_pi(const or_state *st) { return st->pi; }
+const cplx *or_pi_old(const or_state *st) { return st->pi_old; }
+const double *or_res(const or_state *st) { return st->res; }
+const unsigned char *or_active(const or_state *st) { return st->active; }
+const int64_t *or_retired_at(const or_state *st) { return st->retired_at; }
+const cplx *or_y(const or_state *st) { return st->y; }
+const cplx *or_x(const or_state *st, int64_t k) { return st->full ? st->x + k * st->M : NULL; }
+void or_scalars(const or_state *st, cplx *out /* [6] */) {
+    out[0] = st->alpha; out[1] = st->beta; out[2] = st->rho; out[3] = st->w;
+    out[4] = st->zs; out[5] = st->alpha_prev;
+}

@@ -1,0 +1,54 @@
+"""Mutation check of the oracle pins (run by hand: ``python tests/tools/oracle_mutations.py``).
+
+Each mutation is a plausible slip in oracle/shiftk_oracle.c (dropped term, wrong sign, wrong
+index, conjugation, transposed operand).  For each one the oracle is rebuilt and
+tests/test_oracle_pins.py must FAIL.  The original source is always restored.
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+SRC = os.path.join(ROOT, "oracle", "shiftk_oracle.c")
+
+MUTATIONS = [
+    ("- c * st->r_old[i]", "+ c * st->r_old[i]"),                       # sign, EQ-CG-RN-3REC
+    ("rat * rat * beta", "rat * beta"),                                   # EQ-SHIFTEDCG-beta square
+    ("- w - gamma * rho", "- w"),                                         # EQ-REC-ALPHA-N2 term
+    ("- c * st->pi_old[k];", ";"),                                        # EQ-SHIFTEDCG-PI term
+    ("*u = st->g[l] / st->pi[k]", "*u = st->g[l] / pin"),                # P:L373 index
+    ("acc += 0.25 * J * r[s];", "acc += 0.5 * J * r[s];"),               # S^zS^z factor
+    ("(1.0 + cc) * st->t[i] - ac", "(1.0 + c) * st->t[i] - ac"),         # BiCG shadow conj
+    ("st->rho_prev /= fp * fp;", "st->rho_prev /= fp;"),                 # switch transform
+    ("st->alpha_prev *= fp / f;", "st->alpha_prev *= f / fp;"),          # switch transform
+    ("OR_COCG ? dot_plain(st, u, v)", "OR_COCG ? dot_conj(st, u, v)"),   # COCG inner product
+    ("acc += 0.5 * J * r[s2];", "acc += 0.5 * J * r[s];"),               # flip partner
+    ("int j = (i + 1) % L;", "int j = (i + 1 < L) ? i + 1 : i;"),        # periodic bond
+    ("g[l] = dot_conj(st, st->left + l * st->M, v)",
+     "g[l] = dot_plain(st, st->left + l * st->M, v)"),                    # a^dagger projection
+]
+
+
+def main():
+    orig = open(SRC).read()
+    survived = []
+    try:
+        for a, b in MUTATIONS:
+            assert a in orig, a
+            open(SRC, "w").write(orig.replace(a, b, 1))
+            r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q",
+                                os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                               cwd=ROOT, capture_output=True, text=True)
+            caught = r.returncode != 0
+            print(("caught   " if caught else "SURVIVED ") + a + "  ->  " + b, flush=True)
+            if not caught:
+                survived.append(a)
+    finally:
+        open(SRC, "w").write(orig)
+        os.utime(SRC)
+    sys.exit(1 if survived else 0)
+
+
+if __name__ == "__main__":
+    main()
