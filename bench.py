@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark of the shifted-Krylov hot path (one JSON line on rank 0).
+
+A step is one full iteration of shifted COCG/BiCG (seed SpMV with
+fused dot, scalar recurrences + retirement + seed switch, fused three-term update with the
+next-iteration dots and the per-shift projected / full update) over the config's synthetic
+input.  Default workload: C2 (BASELINE.json configs[1]) — Heisenberg L=20, M=2^20, N_z=1024,
+a=b projection, COCG, complex128.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Timing: W untimed iterations, then K iterations each bracketed by CUDA events on the solver's
+stream, with L2 flushed (256 MiB write) before every step outside the events; barrier +
+synchronize around the timed region; max over ranks.  Clocks are sampled with nvidia-smi
+during the timed region.  `--impl reference` times the CPU oracle (oracle/) on the same
+workload (the reference arm of this tier: the paper has no code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "shift-iterations/sec (N_z x iters / s)"
+UNIT = "shift-it/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def bytes_per_row(problem, kernel: str) -> float:
+    """Algorithmic bytes per row of one launch."""
+    nseq = 2 if problem.method == "bicg" else 1
+    if kernel == "spmv":
+        if problem.op["kind"] == "heisenberg":
+            bh = 0.0
+        else:
+            nnz_row = problem.op["col"].shape[0] / problem.M
+            vb = 8 if problem.op["kind"] == "csr_real" else 16
+            bh = nnz_row * (vb + 4) + 8
+        return bh + 32.0 * nseq
+    if kernel == "update":
+        b = 64.0 * nseq + 16.0 * problem.n_left
+        if problem.full_x:
+            b += 64.0 * problem.n_shift   # all shifts active during the timed window
+        return b
+    raise KeyError(kernel)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ oracle legs
+
+def oracle_sample(problem, budget_s: float, max_iters: int):
+    """Time the CPU oracle (as it stands) on the first iterations of the workload."""
+    import oracle
+    o = oracle.Oracle(problem.method, problem.b, problem.z, left=problem.left,
+                      full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax)
+    t0 = time.perf_counter()
+    its = 0
+    while its < max_iters:
+        o.step(problem.op)
+        its += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return its, dt
+
+
+def run_reference(args, problem):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    o = oracle.Oracle(problem.method, problem.b, problem.z, left=problem.left,
+                      full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax)
+    for _ in range(args.warmup):
+        o.step(problem.op)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.step(problem.op)
+    dt = time.perf_counter() - t0
+    val = problem.n_shift * args.steps / dt
+    sample = (f"{problem.name}: oracle iterations {args.warmup}..{args.warmup + args.steps - 1} "
+              f"of the full-size workload (M={problem.M}, N_z={problem.n_shift})")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "config": config_dict(problem, world),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(problem, world):
+    c = {"workload": f"{problem.name}: {synth.CONFIGS[problem.name.split('[')[0]]['desc']}",
+         "M": problem.M, "n_shift": problem.n_shift, "n_left": problem.n_left,
+         "method": problem.method, "full_x": problem.full_x, "parallelism": f"replicas{world}",
+         "l2": "flushed before every timed step (256 MiB write, outside the events)"}
+    return c
+
+
+# ------------------------------------------------------------------------------ GPU leg
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle time")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    rank, world, local = dist_env()
+    problem = synth.make_problem(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, problem)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2001_08707_b200 import shiftk
+    from paper_2001_08707_b200.device import to_device
+
+    dp = to_device(problem, f"cuda:{local}")
+    stream = torch.cuda.Stream()
+    solver = shiftk.Solver(dp.op, problem.method, dp.b, problem.z, left=dp.left,
+                           full_x=problem.full_x, tol=problem.tol, itermax=10 ** 9,
+                           device=local, stream=stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    solver.profile_enable(True)
+    with torch.cuda.stream(stream):
+        solver.enqueue(args.warmup)
+    torch.cuda.synchronize()
+    solver.profile(reset=True)
+    launches0 = solver.profile()["launches"]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xff)
+                starts[i].record(stream)
+                solver.enqueue(1)
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    prof = solver.profile(reset=True)
+    launches = prof["launches"] - launches0
+    coeffs = solver.coefficients()
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = problem.n_shift * args.steps * world / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel (per launch: algorithmic bytes / mean device duration)
+    peak, peak_src = measured_peaks()
+    kernels = {"spmv": prof["ms_spmv"], "update": prof["ms_update"]}
+    dom = max(kernels, key=kernels.get)
+    per_launch_ms = kernels[dom] / max(prof["iterations"], 1)
+    alg_bytes = bytes_per_row(problem, dom) * problem.M
+    achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{problem.name}:{dom}")
+    iter_bytes = (bytes_per_row(problem, "spmv") + bytes_per_row(problem, "update")) * problem.M
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": config_dict(problem, world),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes, "ms_per_launch": per_launch_ms,
+                     "peak_source": peak_src},
+        "kernel_ms_per_step": {k: v / max(prof["iterations"], 1) for k, v in
+                               (("spmv", prof["ms_spmv"]), ("scalar", prof["ms_scalar"]),
+                                ("update", prof["ms_update"]))},
+        "iteration_gbs_model": iter_bytes / (total_ms / args.steps * 1e-3) / 1e9,
+        "gpu_launches": launches,
+        "solver_state": {"iterations": coeffs["iterations"], "n_active": coeffs["n_active"],
+                         "switches": coeffs["switches"]},
+    }
+    line["clocks"] = clk.summary()
+
+    # end-to-end through the public API with HOST buffers (pinned b in, results out)
+    if not args.no_e2e:
+        b_host = torch.from_numpy(problem.b).pin_memory()
+        left_host = None if problem.left is None else torch.from_numpy(problem.left).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s2 = shiftk.Solver(dp.op, problem.method, b_host, problem.z, left=left_host,
+                           full_x=problem.full_x, tol=problem.tol, itermax=10 ** 9, device=local)
+        s2.run(args.steps, poll_every=max(args.steps, 1))
+        y = s2.projections()
+        res = s2.residuals()
+        s2.finalize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        h2d = problem.b.nbytes + problem.z.nbytes + (0 if problem.left is None else problem.left.nbytes)
+        d2h = y.nbytes + res.nbytes
+        line["e2e"] = {"value": problem.n_shift * args.steps * world / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                       "note": "sk_init(host b) + sk_run(K) + sk_get_projection/residual + finalize"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        its, dt = oracle_sample(problem, args.cpu_budget, 400)
+        line["cpu_baseline"] = {"value": problem.n_shift * its / dt, "unit": UNIT, "cores": 1,
+                                "kind": "oracle",
+                                "sample": f"first {its} iterations of {problem.name} (full size), "
+                                          f"{dt:.1f} s single-threaded"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,571 @@
+// api.cu — the C-ABI of libshiftk.so (include/shiftk.h): context lifecycle, iteration
+// enqueueing (single step / CUDA-graph captured loop), getters.  Every step of the method runs in
+// the kernels of kernels.cu; this file only allocates, enqueues and copies.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/shiftk.h"
+#include "kernels.cuh"
+
+static thread_local std::string g_err = "no error";
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return fail(SK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+struct sk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    sk_operator op{};
+    int method = SK_COCG, full = 0, flags = 0;
+    int64_t M = 0;
+    int nz = 0, nl = 0;
+    bool a_is_b = true;
+    double tol = 0, avg_nnz = 0;
+    int64_t itermax = 0;
+    KParams kp{};
+    DevState *st = nullptr;       // device
+    DevState *st_host = nullptr;  // pinned mirror
+    cplx *b = nullptr;            // device copy of b
+    cplx *left_owned = nullptr;
+    std::vector<void *> allocs;
+    cudaGraphExec_t graph = nullptr;
+    int graph_iters = 0;
+    int64_t host_started = 0;     // iterations enqueued (host view, for RC pointers)
+    bool pending_host = false;    // an update ran whose finish phase is not yet enqueued
+    // tracing
+    bool capturing = false;
+    bool profiling = false;
+    int64_t launches = 0;
+    std::vector<cudaEvent_t> ev_pool;  // 4 per profiled iteration
+    size_t ev_used = 0;
+    int64_t prof_iters = 0;
+    double prof_ms[3] = {0, 0, 0};
+};
+
+static cudaError_t prof_mark(sk_ctx *c) {
+    if (!c->profiling || c->capturing) return cudaSuccess;
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r != cudaSuccess) return r;
+        c->ev_pool.push_back(e);
+    }
+    return cudaEventRecord(c->ev_pool[c->ev_used++], c->stream);
+}
+
+static int dalloc(sk_ctx *c, void **p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SK_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + " B): " + cudaGetErrorString(e));
+    }
+    c->allocs.push_back(*p);
+    CK(cudaMemsetAsync(*p, 0, bytes, c->stream));
+    return SK_OK;
+}
+
+static void destroy(sk_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->st_host) cudaFreeHost(c->st_host);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+// --------------------------------------------------------------------------- enqueue helpers
+static int enqueue_spmv(sk_ctx *c) {
+    sk::SpmvArgs a{};
+    a.st = c->st;
+    for (int i = 0; i < 3; ++i) { a.r[i] = c->kp.r[i]; a.t[i] = c->kp.t[i]; }
+    a.q = c->kp.q;
+    a.qt = c->kp.qt;
+    a.part_w = c->kp.part_w;
+    a.M = c->M;
+    a.bicg = c->method == SK_BICG;
+    cudaError_t e;
+    if (c->op.kind == SK_OP_HEISENBERG)
+        e = sk::launch_heisenberg(a, c->op.L, c->op.J, c->kp.nblk_spmv, c->stream);
+    else
+        e = sk::launch_csr(a, c->op.row_ptr, c->op.col, c->op.val, c->op.kind == SK_OP_CSR_CPLX,
+                           c->avg_nnz, c->kp.nblk_spmv, c->stream);
+    CK(e);
+    return SK_OK;
+}
+
+// One iteration: [SpMV] -> scalar(finish previous + start) -> fused update.
+static int enqueue_iteration(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc) {
+    int rc;
+    CK(prof_mark(c));
+    if (q_rc) {
+        CK(sk::launch_rc_dot(c->kp, q_rc, c->stream));
+    } else if ((rc = enqueue_spmv(c)) != SK_OK) {
+        return rc;
+    }
+    CK(prof_mark(c));
+    CK(sk::launch_scalar(c->kp, sk::PH_FINISH | sk::PH_START, c->stream));
+    CK(prof_mark(c));
+    CK(sk::launch_update(c->kp, q_rc ? q_rc : c->kp.q, q_rc ? qt_rc : c->kp.qt, c->stream));
+    CK(prof_mark(c));
+    if (!c->capturing) c->launches += 3;
+    c->host_started += 1;
+    c->pending_host = true;
+    return SK_OK;
+}
+
+static int enqueue_finish(sk_ctx *c) {
+    if (!c->pending_host) return SK_OK;
+    CK(sk::launch_scalar(c->kp, sk::PH_FINISH, c->stream));
+    c->launches += 1;
+    c->pending_host = false;
+    return SK_OK;
+}
+
+static int read_state(sk_ctx *c) {
+    CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+// --------------------------------------------------------------------------- C-ABI
+extern "C" {
+
+const char *sk_last_error(void) { return g_err.c_str(); }
+
+const char *sk_version(void) {
+    return "shiftk 0.1 (sm_100a; shifted COCG/BiCG, Heisenberg + CSR operators)";
+}
+
+int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dist *d) {
+    if (!out || !H || !p) return fail(SK_EINVAL, "null argument");
+    *out = nullptr;
+    const int world = d ? d->world : 1;
+    if (world != 1) return fail(SK_EUNSUPPORTED, "world > 1 is not supported by this build");
+    if (p->method != SK_COCG && p->method != SK_BICG) return fail(SK_EINVAL, "method");
+    if (p->n_shift < 1 || !p->z) return fail(SK_EINVAL, "n_shift >= 1 and z required");
+    if (!(p->tol > 0)) return fail(SK_EINVAL, "tol must be > 0");
+    if (p->itermax < 1) return fail(SK_EINVAL, "itermax must be >= 1");
+    if (!p->b) return fail(SK_EINVAL, "b required");
+    if (p->n_left < 0 || (p->n_left > 0 && !p->left) || (p->n_left == 0 && p->left))
+        return fail(SK_EINVAL, "n_left/left inconsistent");
+    if (p->n_left > 32) return fail(SK_EUNSUPPORTED, "n_left > 32");
+    if (p->n_shift > (1 << 20)) return fail(SK_EUNSUPPORTED, "n_shift > 2^20");
+    const int64_t M = H->M_local > 0 ? H->M_local : H->M;
+    switch (H->kind) {
+        case SK_OP_HEISENBERG:
+            if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L) || M != H->M)
+                return fail(SK_EINVAL, "Heisenberg: need 1 <= L <= 34 and M = M_local = 2^L");
+            break;
+        case SK_OP_CSR_REAL:
+        case SK_OP_CSR_CPLX:
+            if (!H->row_ptr || !H->col || !H->val || M < 1 || H->nnz < 0)
+                return fail(SK_EINVAL, "CSR arrays / sizes");
+            if (M != H->M) return fail(SK_EINVAL, "CSR: M_local must equal M when world == 1");
+            if (H->kind == SK_OP_CSR_CPLX && p->method == SK_COCG)
+                return fail(SK_EUNSUPPORTED,
+                            "COCG needs a complex-symmetric z I - H: use BiCG for complex "
+                            "Hermitian H (Table 1, P:L211-216)");
+            break;
+        case SK_OP_RC:
+            if (M < 1) return fail(SK_EINVAL, "M");
+            break;
+        default:
+            return fail(SK_EINVAL, "operator kind");
+    }
+
+    sk_ctx *c = new (std::nothrow) sk_ctx();
+    if (!c) return fail(SK_ENOMEM, "host allocation");
+    c->device = d ? d->device : 0;
+    c->op = *H;
+    c->method = p->method;
+    c->full = p->full_x ? 1 : 0;
+    c->flags = p->flags;
+    c->M = M;
+    c->nz = (int)p->n_shift;
+    c->a_is_b = p->n_left == 0;
+    c->nl = c->a_is_b ? 1 : (int)p->n_left;
+    c->tol = p->tol;
+    c->itermax = p->itermax;
+    c->avg_nnz = (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) ? double(H->nnz) / double(M) : 0;
+    int rc = SK_OK;
+    auto bail = [&](int code) { destroy(c); return code; };
+
+    if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(SK_ECUDA, "cudaSetDevice"));
+    if (d && d->stream) {
+        c->stream = (cudaStream_t)d->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(SK_ECUDA, "cudaStreamCreate"));
+        c->own_stream = true;
+    }
+    if (cudaMallocHost((void **)&c->st_host, sizeof(DevState)) != cudaSuccess)
+        return bail(fail(SK_ENOMEM, "cudaMallocHost"));
+
+    KParams &kp = c->kp;
+    kp.M = M;
+    kp.nz = c->nz;
+    kp.nl = c->nl;
+    kp.bicg = c->method == SK_BICG;
+    kp.full = c->full;
+    kp.a_is_b = c->a_is_b;
+    kp.flags = c->flags;
+    kp.nblk_spmv = sk::stream_blocks(M);
+    kp.nblk_upd = sk::stream_blocks(M);
+    const size_t vb = (size_t)M * sizeof(cplx);
+
+#define AL(ptr, bytes)                                                                  \
+    do {                                                                                \
+        if ((rc = dalloc(c, (void **)&(ptr), (bytes))) != SK_OK) return bail(rc);       \
+    } while (0)
+    AL(c->st, sizeof(DevState));
+    kp.st = c->st;
+    for (int i = 0; i < 3; ++i) AL(kp.r[i], vb);
+    if (kp.bicg)
+        for (int i = 0; i < 3; ++i) AL(kp.t[i], vb);
+    if (H->kind != SK_OP_RC) {
+        AL(kp.q, vb);
+        if (kp.bicg) AL(kp.qt, vb);
+    }
+    AL(c->b, vb);
+    AL(kp.part_w, sizeof(cplx) * sk::kMaxBlocks);
+    AL(kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
+    cplx *zdev;
+    AL(zdev, sizeof(cplx) * c->nz);
+    kp.z = zdev;
+    AL(kp.pi, sizeof(cplx) * c->nz);
+    AL(kp.pi_old, sizeof(cplx) * c->nz);
+    AL(kp.active, c->nz);
+    AL(kp.res, sizeof(double) * c->nz);
+    AL(kp.retired_at, sizeof(int64_t) * c->nz);
+    AL(kp.u, sizeof(cplx) * c->nz * c->nl);
+    AL(kp.y, sizeof(cplx) * c->nz * c->nl);
+    AL(kp.g, sizeof(cplx) * c->nl);
+    AL(kp.coef, sizeof(cplx) * 3 * c->nz);
+    AL(kp.act_list, sizeof(int32_t) * c->nz);
+    AL(kp.n_act_list, sizeof(int32_t));
+    if (c->full) {
+        AL(kp.p, vb * c->nz);
+        AL(kp.x, vb * c->nz);
+    }
+#undef AL
+
+    // inputs
+    const cudaMemcpyKind kb = p->b_mem == SK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (cudaMemcpyAsync(c->b, p->b, vb, kb, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "copy b"));
+    if (cudaMemcpyAsync(zdev, p->z, sizeof(cplx) * c->nz, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        return bail(fail(SK_ECUDA, "copy z"));
+    if (c->a_is_b) {
+        kp.left = c->b;
+    } else if (p->left_mem == SK_MEM_DEVICE) {
+        kp.left = (const cplx *)p->left;
+    } else {
+        if ((rc = dalloc(c, (void **)&c->left_owned, vb * c->nl)) != SK_OK) return bail(rc);
+        if (cudaMemcpyAsync(c->left_owned, p->left, vb * c->nl, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+            return bail(fail(SK_ECUDA, "copy left"));
+        kp.left = c->left_owned;
+    }
+    // per-shift init: pi_0 = pi_{-1} = 1, active, retired_at = -1
+    {
+        std::vector<cplx> ones(c->nz, mk(1.0, 0.0));
+        std::vector<uint8_t> act(c->nz, 1);
+        std::vector<int64_t> ret(c->nz, -1);
+        if (cudaMemcpyAsync(kp.pi, ones.data(), sizeof(cplx) * c->nz, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(kp.pi_old, ones.data(), sizeof(cplx) * c->nz, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(kp.active, act.data(), c->nz, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(kp.retired_at, ret.data(), sizeof(int64_t) * c->nz, cudaMemcpyHostToDevice, c->stream))
+            return bail(fail(SK_ECUDA, "init per-shift arrays"));
+        DevState h{};
+        h.status = 0;
+        h.seed = 0;
+        h.n_active = c->nz;
+        h.zs = mk(p->z[0].re, p->z[0].im);
+        h.sr_cur = mk(1, 0);
+        h.sr_prev = mk(1, 0);
+        h.tol = c->tol;
+        h.itermax = c->itermax;
+        *c->st_host = h;
+        if (cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream))
+            return bail(fail(SK_ECUDA, "init state"));
+        // the pinned mirror is reused below; make sure the copy has consumed it
+        if (cudaStreamSynchronize(c->stream)) return bail(fail(SK_ECUDA, "sync"));
+    }
+    if (sk::launch_init(kp, c->b, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init kernel"));
+    if (sk::launch_scalar(kp, sk::PH_INIT, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init scalar"));
+    if ((rc = read_state(c)) != SK_OK) return bail(rc);
+    if (!(c->st_host->nu > 0)) return bail(fail(SK_EINVAL, "||b|| must be > 0"));
+    *out = c;
+    return SK_OK;
+}
+
+int sk_update(sk_ctx *c, int32_t *status) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    if (c->op.kind == SK_OP_RC) return fail(SK_ESTATE, "SK_OP_RC context: use sk_update_rc");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = enqueue_iteration(c, nullptr, nullptr)) != SK_OK) return rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    if (status) *status = c->st_host->status;
+    return SK_OK;
+}
+
+int sk_update_rc(sk_ctx *c, const sk_cplx *q, const sk_cplx *qt, int32_t *status) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    if (!q || (c->method == SK_BICG && !qt)) return fail(SK_EINVAL, "q (and qt for BiCG) required");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = enqueue_iteration(c, (const cplx *)q, (const cplx *)qt)) != SK_OK) return rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    if (status) *status = c->st_host->status;
+    return SK_OK;
+}
+
+int sk_get_seed_vectors(sk_ctx *c, const sk_cplx **r, const sk_cplx **rt) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    const int64_t i = c->st_host->n_started % 3;
+    if (r) *r = (const sk_cplx *)c->kp.r[i];
+    if (rt) *rt = c->method == SK_BICG ? (const sk_cplx *)c->kp.t[i] : nullptr;
+    return SK_OK;
+}
+
+static int capture_graph(sk_ctx *c, int iters) {
+    if (c->graph && c->graph_iters == iters) return SK_OK;
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t hs = c->host_started;
+    const bool ph = c->pending_host;
+    int rc = SK_OK;
+    c->capturing = true;
+    for (int i = 0; i < iters && rc == SK_OK; ++i) rc = enqueue_iteration(c, nullptr, nullptr);
+    c->capturing = false;
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->host_started = hs;
+    c->pending_host = ph;
+    if (rc != SK_OK) return rc;
+    CK(e);
+    e = cudaGraphInstantiate(&c->graph, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    c->graph_iters = iters;
+    return SK_OK;
+}
+
+// Enqueue `iters` iterations: full graph chunks, then single iterations.
+static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk) {
+    int rc;
+    if (c->profiling) chunk = 1;   // individual launches bracketed by events
+    if (iters >= chunk && chunk > 1) {
+        if ((rc = capture_graph(c, chunk)) != SK_OK) return rc;
+    }
+    while (iters >= chunk && chunk > 1) {
+        CK(cudaGraphLaunch(c->graph, c->stream));
+        c->launches += 3 * chunk;
+        c->host_started += chunk;
+        c->pending_host = true;
+        iters -= chunk;
+    }
+    while (iters-- > 0)
+        if ((rc = enqueue_iteration(c, nullptr, nullptr)) != SK_OK) return rc;
+    return SK_OK;
+}
+
+int sk_run(sk_ctx *c, int64_t max_iters, int32_t poll_every, int32_t *status) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    if (c->op.kind == SK_OP_RC) return fail(SK_ESTATE, "SK_OP_RC context: use sk_update_rc");
+    if (max_iters < 0) return fail(SK_EINVAL, "max_iters < 0");
+    CK(cudaSetDevice(c->device));
+    if (poll_every <= 0) poll_every = 64;
+    const int chunk = poll_every < 16 ? poll_every : 16;
+    int rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    int64_t left = max_iters;
+    while (left > 0 && c->st_host->status == SK_ITERATING) {
+        const int64_t now = left < poll_every ? left : poll_every;
+        if ((rc = enqueue_iters(c, now, chunk)) != SK_OK) return rc;
+        left -= now;
+        // status visible after the next finish: copy asynchronously (finish pending iteration)
+        if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+        if ((rc = read_state(c)) != SK_OK) return rc;
+    }
+    if (status) *status = c->st_host->status;
+    return SK_OK;
+}
+
+int sk_enqueue(sk_ctx *c, int64_t iters) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    if (c->op.kind == SK_OP_RC) return fail(SK_ESTATE, "SK_OP_RC context: use sk_update_rc");
+    if (iters < 0) return fail(SK_EINVAL, "iters < 0");
+    CK(cudaSetDevice(c->device));
+    return enqueue_iters(c, iters, 16);
+}
+
+int sk_get_residual(sk_ctx *c, double *res) {
+    if (!c || !res) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    CK(cudaMemcpyAsync(res, c->kp.res, sizeof(double) * c->nz, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+int sk_get_projection(sk_ctx *c, sk_cplx *y) {
+    if (!c || !y) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    CK(cudaMemcpyAsync(y, c->kp.y, sizeof(cplx) * c->nz * c->nl, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+int sk_get_solution(sk_ctx *c, int64_t k, const sk_cplx **x) {
+    if (!c || !x) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (!c->full) return fail(SK_ESTATE, "context was created without full_x");
+    if (k < 0 || k >= c->nz) return fail(SK_EINVAL, "shift index out of range");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    *x = (const sk_cplx *)(c->kp.x + k * c->M);
+    return SK_OK;
+}
+
+int sk_copy_solution(sk_ctx *c, int64_t k, sk_cplx *dst, int32_t dst_mem) {
+    if (!c || !dst) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (!c->full) return fail(SK_ESTATE, "context was created without full_x");
+    if (k < 0 || k >= c->nz) return fail(SK_EINVAL, "shift index out of range");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    CK(cudaMemcpyAsync(dst, c->kp.x + k * c->M, sizeof(cplx) * c->M,
+                       dst_mem == SK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+int sk_get_shift_state(sk_ctx *c, sk_cplx *pi, uint8_t *active, int64_t *retired_at) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if (pi) CK(cudaMemcpyAsync(pi, c->kp.pi, sizeof(cplx) * c->nz, cudaMemcpyDeviceToHost, c->stream));
+    if (active) CK(cudaMemcpyAsync(active, c->kp.active, c->nz, cudaMemcpyDeviceToHost, c->stream));
+    if (retired_at)
+        CK(cudaMemcpyAsync(retired_at, c->kp.retired_at, sizeof(int64_t) * c->nz, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+int sk_get_coefficients(sk_ctx *c, sk_coeffs *o) {
+    if (!c || !o) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    const DevState &h = *c->st_host;
+    o->iterations = h.n;
+    o->seed_index = h.seed;
+    o->switches = h.nswitch;
+    o->spmv_count = h.nspmv;
+    o->n_active = h.n_active;
+    o->status = h.status;
+    o->reserved = 0;
+    o->z_seed = {h.zs.x, h.zs.y};
+    o->alpha = {h.alpha_prev.x, h.alpha_prev.y};
+    o->rho = {h.rho_prev.x, h.rho_prev.y};
+    o->beta = {h.beta.x, h.beta.y};
+    o->seed_residual = h.nu;
+    return SK_OK;
+}
+
+int sk_profile_enable(sk_ctx *c, int32_t on) {
+    if (!c) return fail(SK_ESTATE, "null context");
+    c->profiling = on != 0;
+    return SK_OK;
+}
+
+int sk_get_profile(sk_ctx *c, sk_profile *o, int32_t reset) {
+    if (!c || !o) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    CK(cudaStreamSynchronize(c->stream));
+    // events come in groups of 4 per iteration: [spmv] [scalar] [update]
+    const size_t groups = c->ev_used / 4;
+    for (size_t i = 0; i < groups; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, c->ev_pool[4 * i + k], c->ev_pool[4 * i + k + 1]));
+            c->prof_ms[k] += ms;
+        }
+    }
+    c->prof_iters += (int64_t)groups;
+    c->ev_used = 0;
+    o->iterations = c->prof_iters;
+    o->launches = c->launches;
+    o->ms_spmv = c->prof_ms[0];
+    o->ms_scalar = c->prof_ms[1];
+    o->ms_update = c->prof_ms[2];
+    if (reset) {
+        c->prof_iters = 0;
+        c->prof_ms[0] = c->prof_ms[1] = c->prof_ms[2] = 0;
+    }
+    return SK_OK;
+}
+
+int sk_finalize(sk_ctx **pc) {
+    if (!pc || !*pc) return fail(SK_ESTATE, "sk_finalize on a null / finalized context");
+    destroy(*pc);
+    *pc = nullptr;
+    return SK_OK;
+}
+
+int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *stream) {
+    if (!H || !r || !q) return fail(SK_EINVAL, "null argument");
+    sk::SpmvArgs a{};
+    a.st = nullptr;
+    a.r[0] = (const cplx *)r;
+    a.q = (cplx *)q;
+    a.part_w = nullptr;
+    a.bicg = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (H->kind == SK_OP_HEISENBERG) {
+        if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L)) return fail(SK_EINVAL, "L/M");
+        a.M = H->M;
+        CK(sk::launch_heisenberg(a, H->L, H->J, sk::stream_blocks(a.M), s));
+    } else if (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) {
+        const int64_t M = H->M_local > 0 ? H->M_local : H->M;
+        if (!H->row_ptr || !H->col || !H->val || M < 1) return fail(SK_EINVAL, "CSR");
+        a.M = M;
+        CK(sk::launch_csr(a, H->row_ptr, H->col, H->val, H->kind == SK_OP_CSR_CPLX,
+                          double(H->nnz) / double(M), sk::stream_blocks(M), s));
+    } else {
+        return fail(SK_EINVAL, "operator kind");
+    }
+    return SK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// common.cuh — device-side types and complex fp64 helpers shared by the CUDA kernels of
+// libshiftk.so.  (The CPU oracle in oracle/ shares nothing with this file.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+typedef double2 cplx;  // (x = re, y = im), 16-byte aligned -> LDG.128 / STG.128
+
+__host__ __device__ __forceinline__ cplx mk(double re, double im) { return make_double2(re, im); }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return mk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return mk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+    return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return mk(a.x, -a.y); }
+__host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return mk(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+__host__ __device__ __forceinline__ double cabsd(cplx a) { return hypot(a.x, a.y); }
+// a * conj-free fused: acc += a * b
+__host__ __device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx acc) {
+    return mk(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+// acc += conj(a) * b
+__host__ __device__ __forceinline__ cplx cfma_conj(cplx a, cplx b, cplx acc) {
+    return mk(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y)));
+}
+// Smith's algorithm: a / b without needless overflow/underflow.
+__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+    if (fabs(b.x) >= fabs(b.y)) {
+        double r = b.y / b.x, d = b.x + b.y * r;
+        return mk((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+    } else {
+        double r = b.x / b.y, d = b.x * r + b.y;
+        return mk((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+    }
+}
+__host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(mk(1.0, 0.0), b); }
+
+__device__ __forceinline__ cplx ldg_cs(const cplx *p) {  // streaming load (read once)
+    return __ldcs(p);
+}
+__device__ __forceinline__ void stg_cs(cplx *p, cplx v) { __stcs(p, v); }
+
+__device__ __forceinline__ cplx warp_sum(cplx v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    return v;
+}
+
+// Deterministic block sum of NV complex values per thread; result valid in thread 0.
+// scratch: >= NV * (blockDim.x/32) cplx in shared memory.
+template <int NV>
+__device__ __forceinline__ void block_sum(cplx (&v)[NV], cplx *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+    if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) scratch[j * nw + warp] = v[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            cplx s = scratch[j * nw];
+            for (int w = 1; w < nw; ++w) s = cadd(s, scratch[j * nw + w]);
+            v[j] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Device-resident solver state (one per context).  Everything a kernel needs per iteration is
+// read from here, so a captured CUDA graph can replay iterations without host involvement.
+// ---------------------------------------------------------------------------------------------
+struct DevState {
+    int64_t n;           // completed iterations
+    int64_t n_started;   // iterations whose seed/shift scalar step ran (buffer rotation index)
+    int64_t nswitch;
+    int64_t nspmv;
+    int32_t status;      // sk_status
+    int32_t pending;     // 1: update(n) ran, finish(n) not yet
+    int32_t seed;        // current seed index s
+    int32_t n_active;
+    cplx zs;             // seed shift z_s
+    cplx alpha_prev;     // alpha_{n-1} (current-seed normalisation)
+    cplx rho_cur;        // rho_n of the current r_n (current-seed normalisation)
+    cplx rho_prev;       // rho_{n-1}
+    cplx sr_cur, sr_prev;   // lazy scale: r_true = sr * r_stored (shadow: conj(sr))
+    cplx a_cur, a_q, a_prev; // r_{n+1} = a_cur r_cur_st + a_q q_raw + a_prev r_prev_st
+    double nu;           // ||r_n||_2 (true scale)
+    double tol;
+    int64_t itermax;
+    // diagnostics of the last iteration
+    cplx alpha, beta, w;
+};
+
+// Pointers/sizes passed by value to every kernel.
+struct KParams {
+    DevState *st;
+    int64_t M;           // local rows
+    int32_t nz, nl;      // shifts, projections
+    int32_t bicg, full;
+    int32_t a_is_b;
+    int32_t flags;
+    cplx *r[3];          // rotating seed residual buffers, r_n = r[n_started % 3] before start(n)
+    cplx *t[3];          // shadow (BiCG)
+    cplx *q, *qt;        // H r, H t (raw, i.e. applied to stored vectors)
+    const cplx *left;    // [nl][M] (== b when a = b)
+    cplx *part_w;        // [nblk_spmv]
+    cplx *part_u;        // [nblk_upd][2 + nl]
+    int32_t nblk_spmv, nblk_upd;
+    // per-shift arrays [nz]
+    const cplx *z;
+    cplx *pi, *pi_old;
+    uint8_t *active;
+    double *res;
+    int64_t *retired_at;
+    cplx *u, *y;         // [nz][nl]
+    cplx *g;             // [nl] projection of current r (true scale)
+    // full mode
+    cplx *p, *x;         // [nz][M]
+    cplx *coef;          // [nz][3]: (sr/pi_n, beta^k_{n-1}, alpha^k_n) for active list order
+    int32_t *act_list;   // [nz]
+    int32_t *n_act_list; // [1]
+};

@@ -1,0 +1,300 @@
+"""Thin ctypes binding of libshiftk.so (include/shiftk.h).  Argument marshalling only: every
+step of the method runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+library or a CUDA device is missing, loading fails loudly.
+
+Names follow the C-ABI (sk_init / sk_update / sk_run / sk_get_* / sk_finalize), which follows
+the paper's init / update / getresidual / finalize flow (Alg. 1
+P:L529-552).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libshiftk.so")
+
+COCG, BICG = 0, 1
+OP_HEISENBERG, OP_CSR_REAL, OP_CSR_CPLX, OP_RC = 0, 1, 2, 3
+ITERATING, CONVERGED, MAXITER, BREAKDOWN = 0, 1, 2, 3
+STATUS_NAMES = {0: "iterating", 1: "converged", 2: "maxiter", 3: "breakdown"}
+MEM_HOST, MEM_DEVICE = 0, 1
+FLAG_NO_SWITCH = 1
+ERRORS = {0: "SK_OK", -1: "SK_EINVAL", -2: "SK_ENOMEM", -3: "SK_ECUDA", -4: "SK_ENCCL",
+          -5: "SK_ESTATE", -6: "SK_EUNSUPPORTED"}
+EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_run", "sk_enqueue",
+           "sk_get_residual", "sk_get_projection", "sk_get_solution", "sk_get_shift_state",
+           "sk_get_coefficients", "sk_finalize", "sk_apply_operator", "sk_last_error", "sk_version",
+           "sk_profile_enable", "sk_get_profile", "sk_copy_solution"]
+
+
+class ShiftkError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn} -> {ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class sk_cplx(ctypes.Structure):
+    _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
+
+
+class sk_operator(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("L", ctypes.c_int32), ("J", ctypes.c_double),
+                ("M", ctypes.c_int64), ("M_local", ctypes.c_int64), ("row_begin", ctypes.c_int64),
+                ("nnz", ctypes.c_int64), ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("val", ctypes.c_void_p)]
+
+
+class sk_params(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("flags", ctypes.c_int32), ("n_shift", ctypes.c_int64),
+                ("z", ctypes.c_void_p), ("b", ctypes.c_void_p), ("b_mem", ctypes.c_int32),
+                ("left_mem", ctypes.c_int32), ("n_left", ctypes.c_int64), ("left", ctypes.c_void_p),
+                ("full_x", ctypes.c_int32), ("tol", ctypes.c_double), ("itermax", ctypes.c_int64)]
+
+
+class sk_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class sk_coeffs(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("seed_index", ctypes.c_int64),
+                ("switches", ctypes.c_int64), ("spmv_count", ctypes.c_int64),
+                ("n_active", ctypes.c_int64), ("status", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("z_seed", sk_cplx), ("alpha", sk_cplx), ("rho", sk_cplx), ("beta", sk_cplx),
+                ("seed_residual", ctypes.c_double)]
+
+
+class sk_profile(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("ms_spmv", ctypes.c_double), ("ms_scalar", ctypes.c_double),
+                ("ms_update", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libshiftk.so (no fallback: raises if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(path)
+    P, I64, I32, VP = ctypes.POINTER, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    sig = {
+        "sk_init": [P(VP), P(sk_operator), P(sk_params), P(sk_dist)],
+        "sk_update": [VP, P(I32)],
+        "sk_update_rc": [VP, VP, VP, P(I32)],
+        "sk_get_seed_vectors": [VP, P(VP), P(VP)],
+        "sk_run": [VP, I64, I32, P(I32)],
+        "sk_enqueue": [VP, I64],
+        "sk_get_residual": [VP, VP],
+        "sk_get_projection": [VP, VP],
+        "sk_get_solution": [VP, I64, P(VP)],
+        "sk_get_shift_state": [VP, VP, VP, VP],
+        "sk_get_coefficients": [VP, P(sk_coeffs)],
+        "sk_finalize": [P(VP)],
+        "sk_apply_operator": [P(sk_operator), VP, VP, VP],
+        "sk_profile_enable": [VP, I32],
+        "sk_copy_solution": [VP, I64, VP, I32],
+        "sk_get_profile": [VP, P(sk_profile), I32],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.sk_last_error.restype = ctypes.c_char_p
+    L.sk_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(code: int, fn: str):
+    if code != 0:
+        raise ShiftkError(code, fn, load().sk_last_error().decode())
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr_mem(a):
+    """(pointer, sk_mem) of a numpy array (host) or a torch tensor (host or cuda)."""
+    if a is None:
+        return None, MEM_HOST
+    if _is_torch(a):
+        assert a.is_contiguous()
+        return a.data_ptr(), (MEM_DEVICE if a.is_cuda else MEM_HOST)
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous
+    return a.ctypes.data, MEM_HOST
+
+
+def make_operator(op: dict, M: int, dev_arrays: Optional[dict] = None) -> sk_operator:
+    """Build sk_operator from a synth op dict; CSR arrays must be given as device tensors in
+    ``dev_arrays`` (row_ptr int64, col int32, val float64/complex128)."""
+    o = sk_operator()
+    o.M = M
+    o.M_local = M
+    o.row_begin = 0
+    if op["kind"] == "heisenberg":
+        o.kind, o.L, o.J = OP_HEISENBERG, int(op["L"]), float(op["J"])
+    elif op["kind"] in ("csr_real", "csr_cplx"):
+        o.kind = OP_CSR_REAL if op["kind"] == "csr_real" else OP_CSR_CPLX
+        d = dev_arrays
+        o.row_ptr, o.col, o.val = d["row_ptr"].data_ptr(), d["col"].data_ptr(), d["val"].data_ptr()
+        o.nnz = int(d["col"].numel())
+    elif op["kind"] == "rc":
+        o.kind = OP_RC
+    else:
+        raise ValueError(op["kind"])
+    return o
+
+
+class _CudaView:
+    """__cuda_array_interface__ wrapper so torch.as_tensor can view a library-owned buffer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<c16", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, n: int):
+    """torch complex128 view (no copy) of n elements at a library device pointer."""
+    import torch
+    return torch.as_tensor(_CudaView(ptr, n), device="cuda")
+
+
+def apply_operator(op: sk_operator, r_dev, q_dev, stream: int = 0):
+    """q = H r on device tensors (complex128)."""
+    _check(load().sk_apply_operator(ctypes.byref(op), r_dev.data_ptr(), q_dev.data_ptr(),
+                                    ctypes.c_void_p(stream)), "sk_apply_operator")
+
+
+class Solver:
+    """One sk_ctx.  ``b``/``left`` may be numpy arrays (host; copied) or torch tensors (device:
+    b copied, left borrowed).  ``op`` is an sk_operator (keep its device arrays alive)."""
+
+    def __init__(self, op: sk_operator, method: str, b, z: np.ndarray, *, left=None,
+                 full_x: bool = False, tol: float = 1e-10, itermax: int = 10000, flags: int = 0,
+                 device: int = 0, stream: int = 0):
+        L = load()
+        self._keep = [op, b, left]
+        self.z = np.ascontiguousarray(z, dtype=np.complex128)
+        self.nz = int(self.z.shape[0])
+        self.nl = 1 if left is None else int(left.shape[0])
+        self.full_x = bool(full_x)
+        p = sk_params()
+        p.method = COCG if method == "cocg" else BICG
+        p.flags = flags
+        p.n_shift = self.nz
+        p.z = self.z.ctypes.data
+        p.b, p.b_mem = _ptr_mem(b)
+        if left is None:
+            p.n_left, p.left, p.left_mem = 0, None, MEM_HOST
+        else:
+            p.left, p.left_mem = _ptr_mem(left)
+            p.n_left = self.nl
+        p.full_x = int(full_x)
+        p.tol = tol
+        p.itermax = itermax
+        d = sk_dist()
+        d.rank, d.world, d.device = 0, 1, device
+        d.nccl_id, d.stream = None, stream or None
+        self._h = ctypes.c_void_p()
+        _check(L.sk_init(ctypes.byref(self._h), ctypes.byref(op), ctypes.byref(p), ctypes.byref(d)),
+               "sk_init")
+        self.M = int(op.M_local)
+
+    # -- iteration ---------------------------------------------------------------------
+    def update(self) -> int:
+        st = ctypes.c_int32()
+        _check(load().sk_update(self._h, ctypes.byref(st)), "sk_update")
+        return st.value
+
+    def update_rc(self, q_dev, qt_dev=None) -> int:
+        st = ctypes.c_int32()
+        _check(load().sk_update_rc(self._h, q_dev.data_ptr(),
+                                   None if qt_dev is None else qt_dev.data_ptr(), ctypes.byref(st)),
+               "sk_update_rc")
+        return st.value
+
+    def seed_vectors(self):
+        r, t = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(load().sk_get_seed_vectors(self._h, ctypes.byref(r), ctypes.byref(t)), "sk_get_seed_vectors")
+        return r.value, t.value
+
+    def run(self, max_iters: int, poll_every: int = 64) -> int:
+        st = ctypes.c_int32()
+        _check(load().sk_run(self._h, max_iters, poll_every, ctypes.byref(st)), "sk_run")
+        return st.value
+
+    def enqueue(self, iters: int):
+        _check(load().sk_enqueue(self._h, iters), "sk_enqueue")
+
+    # -- results -------------------------------------------------------------------------
+    def residuals(self) -> np.ndarray:
+        out = np.empty(self.nz, dtype=np.float64)
+        _check(load().sk_get_residual(self._h, out.ctypes.data), "sk_get_residual")
+        return out
+
+    def projections(self) -> np.ndarray:
+        out = np.empty((self.nz, self.nl), dtype=np.complex128)
+        _check(load().sk_get_projection(self._h, out.ctypes.data), "sk_get_projection")
+        return out
+
+    def solution_ptr(self, k: int) -> int:
+        x = ctypes.c_void_p()
+        _check(load().sk_get_solution(self._h, k, ctypes.byref(x)), "sk_get_solution")
+        return x.value
+
+    def solution(self, k: int) -> np.ndarray:
+        """x^(k) copied to host (full mode)."""
+        out = np.empty(self.M, dtype=np.complex128)
+        _check(load().sk_copy_solution(self._h, k, out.ctypes.data, MEM_HOST), "sk_copy_solution")
+        return out
+
+    def shift_state(self):
+        pi = np.empty(self.nz, dtype=np.complex128)
+        act = np.empty(self.nz, dtype=np.uint8)
+        ret = np.empty(self.nz, dtype=np.int64)
+        _check(load().sk_get_shift_state(self._h, pi.ctypes.data, act.ctypes.data, ret.ctypes.data),
+               "sk_get_shift_state")
+        return pi, act.astype(bool), ret
+
+    def coefficients(self) -> dict:
+        c = sk_coeffs()
+        _check(load().sk_get_coefficients(self._h, ctypes.byref(c)), "sk_get_coefficients")
+        cz = lambda v: complex(v.re, v.im)
+        return dict(iterations=c.iterations, seed_index=c.seed_index, switches=c.switches,
+                    spmv_count=c.spmv_count, n_active=c.n_active, status=c.status,
+                    z_seed=cz(c.z_seed), alpha=cz(c.alpha), rho=cz(c.rho), beta=cz(c.beta),
+                    seed_residual=c.seed_residual)
+
+    def profile_enable(self, on: bool = True):
+        _check(load().sk_profile_enable(self._h, int(on)), "sk_profile_enable")
+
+    def profile(self, reset: bool = False) -> dict:
+        p = sk_profile()
+        _check(load().sk_get_profile(self._h, ctypes.byref(p), int(reset)), "sk_get_profile")
+        return dict(iterations=p.iterations, launches=p.launches, ms_spmv=p.ms_spmv,
+                    ms_scalar=p.ms_scalar, ms_update=p.ms_update)
+
+    @property
+    def iterations(self) -> int:
+        return self.coefficients()["iterations"]
+
+    def finalize(self):
+        if self._h and self._h.value:
+            _check(load().sk_finalize(ctypes.byref(self._h)), "sk_finalize")
+        self._keep = []
+
+    def __del__(self):
+        try:
+            self.finalize()
+        except Exception:
+            pass
