@@ -220,6 +220,11 @@ int sk_profile_enable(sk_ctx *ctx, int32_t on);
 /* Synchronises the stream, accumulates the recorded events into *out; reset != 0 clears. */
 int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
 
+/* Diagnostics: %globaltimer stamps (ns) written by the last scalar-step kernel at its phase
+   boundaries [0 entry, 1 inputs staged, 2 finish done, 5 seed scalars, 6 compaction,
+   3 start done, 4 exit].  Requires the environment variable SHIFTK_DEBUG_TS at sk_init. */
+int sk_debug_timestamps(sk_ctx *ctx, int64_t *out16);
+
 /* Library version / build info string (never NULL). */
 const char *sk_version(void);
 

@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -229,45 +230,58 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.full = c->full;
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
-    kp.nblk_spmv = sk::stream_blocks(M);
+    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M) : sk::stream_blocks(M);
     kp.nblk_upd = sk::stream_blocks(M);
     const size_t vb = (size_t)M * sizeof(cplx);
 
-#define AL(ptr, bytes)                                                                  \
-    do {                                                                                \
-        if ((rc = dalloc(c, (void **)&(ptr), (bytes))) != SK_OK) return bail(rc);       \
-    } while (0)
-    AL(c->st, sizeof(DevState));
+    // One device arena for everything the context owns (one cudaMalloc / cudaFree); every
+    // array is padded to 256 B so bulk (TMA) copies of rounded sizes stay inside it.
+    cplx *zdev = nullptr;
+    {
+        struct Item { void **p; size_t bytes; };
+        std::vector<Item> items;
+        auto add = [&](void *pp, size_t bytes) { items.push_back({(void **)pp, bytes}); };
+        add(&c->st, sizeof(DevState));
+        for (int i = 0; i < 3; ++i) add(&kp.r[i], vb);
+        if (kp.bicg)
+            for (int i = 0; i < 3; ++i) add(&kp.t[i], vb);
+        if (H->kind != SK_OP_RC) {
+            add(&kp.q, vb);
+            if (kp.bicg) add(&kp.qt, vb);
+        }
+        add(&c->b, vb);
+        add(&kp.part_w, sizeof(cplx) * sk::kMaxBlocks);
+        add(&kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
+        add(&zdev, sizeof(cplx) * c->nz);
+        add(&kp.pi, sizeof(cplx) * c->nz);
+        add(&kp.pi_old, sizeof(cplx) * c->nz);
+        add(&kp.active, c->nz);
+        add(&kp.res, sizeof(double) * c->nz);
+        add(&kp.retired_at, sizeof(int64_t) * c->nz);
+        add(&kp.u, sizeof(cplx) * c->nz * c->nl);
+        add(&kp.y, sizeof(cplx) * c->nz * c->nl);
+        add(&kp.g, sizeof(cplx) * c->nl);
+        add(&kp.coef, sizeof(cplx) * 3 * c->nz);
+        add(&kp.act_list, sizeof(int32_t) * c->nz);
+        add(&kp.n_act_list, sizeof(int32_t));
+        if (getenv("SHIFTK_DEBUG_TS")) add(&kp.dbg_ts, sizeof(int64_t) * 16);
+        if (!c->a_is_b && p->left_mem != SK_MEM_DEVICE) add(&c->left_owned, vb * c->nl);
+        if (c->full) {
+            add(&kp.p, vb * c->nz);
+            add(&kp.x, vb * c->nz);
+        }
+        size_t total = 0;
+        for (auto &it : items) total += (it.bytes + 255) & ~size_t(255);
+        void *arena = nullptr;
+        if ((rc = dalloc(c, &arena, total)) != SK_OK) return bail(rc);
+        size_t off = 0;
+        for (auto &it : items) {
+            *it.p = (char *)arena + off;
+            off += (it.bytes + 255) & ~size_t(255);
+        }
+    }
     kp.st = c->st;
-    for (int i = 0; i < 3; ++i) AL(kp.r[i], vb);
-    if (kp.bicg)
-        for (int i = 0; i < 3; ++i) AL(kp.t[i], vb);
-    if (H->kind != SK_OP_RC) {
-        AL(kp.q, vb);
-        if (kp.bicg) AL(kp.qt, vb);
-    }
-    AL(c->b, vb);
-    AL(kp.part_w, sizeof(cplx) * sk::kMaxBlocks);
-    AL(kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
-    cplx *zdev;
-    AL(zdev, sizeof(cplx) * c->nz);
     kp.z = zdev;
-    AL(kp.pi, sizeof(cplx) * c->nz);
-    AL(kp.pi_old, sizeof(cplx) * c->nz);
-    AL(kp.active, c->nz);
-    AL(kp.res, sizeof(double) * c->nz);
-    AL(kp.retired_at, sizeof(int64_t) * c->nz);
-    AL(kp.u, sizeof(cplx) * c->nz * c->nl);
-    AL(kp.y, sizeof(cplx) * c->nz * c->nl);
-    AL(kp.g, sizeof(cplx) * c->nl);
-    AL(kp.coef, sizeof(cplx) * 3 * c->nz);
-    AL(kp.act_list, sizeof(int32_t) * c->nz);
-    AL(kp.n_act_list, sizeof(int32_t));
-    if (c->full) {
-        AL(kp.p, vb * c->nz);
-        AL(kp.x, vb * c->nz);
-    }
-#undef AL
 
     // inputs
     const cudaMemcpyKind kb = p->b_mem == SK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -279,7 +293,6 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     } else if (p->left_mem == SK_MEM_DEVICE) {
         kp.left = (const cplx *)p->left;
     } else {
-        if ((rc = dalloc(c, (void **)&c->left_owned, vb * c->nl)) != SK_OK) return bail(rc);
         if (cudaMemcpyAsync(c->left_owned, p->left, vb * c->nl, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
             return bail(fail(SK_ECUDA, "copy left"));
         kp.left = c->left_owned;
@@ -536,6 +549,14 @@ int sk_get_profile(sk_ctx *c, sk_profile *o, int32_t reset) {
     return SK_OK;
 }
 
+int sk_debug_timestamps(sk_ctx *c, int64_t *out16) {
+    if (!c || !out16) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (!c->kp.dbg_ts) return fail(SK_ESTATE, "set SHIFTK_DEBUG_TS before sk_init");
+    CK(cudaMemcpyAsync(out16, c->kp.dbg_ts, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
 int sk_finalize(sk_ctx **pc) {
     if (!pc || !*pc) return fail(SK_ESTATE, "sk_finalize on a null / finalized context");
     destroy(*pc);
@@ -555,7 +576,7 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
     if (H->kind == SK_OP_HEISENBERG) {
         if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L)) return fail(SK_EINVAL, "L/M");
         a.M = H->M;
-        CK(sk::launch_heisenberg(a, H->L, H->J, sk::stream_blocks(a.M), s));
+        CK(sk::launch_heisenberg(a, H->L, H->J, sk::heisenberg_blocks(H->L, a.M), s));
     } else if (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) {
         const int64_t M = H->M_local > 0 ? H->M_local : H->M;
         if (!H->row_ptr || !H->col || !H->val || M < 1) return fail(SK_EINVAL, "CSR");

@@ -42,6 +42,14 @@ __device__ __forceinline__ cplx ldg_cs(const cplx *p) {  // streaming load (read
 }
 __device__ __forceinline__ void stg_cs(cplx *p, cplx v) { __stcs(p, v); }
 
+__device__ __forceinline__ void dbg_stamp(int64_t *ts, int i) {
+    if (ts && threadIdx.x == 0) {
+        int64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ts[i] = t;
+    }
+}
+
 __device__ __forceinline__ cplx warp_sum(cplx v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -128,4 +136,5 @@ struct KParams {
     cplx *coef;          // [nz][3]: (sr/pi_n, beta^k_{n-1}, alpha^k_n) for active list order
     int32_t *act_list;   // [nz]
     int32_t *n_act_list; // [1]
+    int64_t *dbg_ts;     // optional [16] %globaltimer stamps of the scalar kernel phases
 };

@@ -14,6 +14,8 @@
 //
 // All reductions are two-stage and deterministic: each CTA reduces its grid-stride rows in a
 // fixed order, the scalar kernel sums the CTA partials in CTA order.
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace sk {
@@ -25,6 +27,14 @@ template <typename T>
 __device__ __forceinline__ T pick3(T const (&a)[3], int64_t i) {
     const int k = (int)(i % 3);
     return k == 0 ? a[0] : (k == 1 ? a[1] : a[2]);
+}
+
+int heisenberg_blocks(int L, int64_t M) {
+    if (L > kTileBitsPublic && L <= 34) {
+        const int64_t ntiles = M >> kTileBitsPublic;
+        return (int)(ntiles < (int64_t)kMaxBlocks ? ntiles : (int64_t)kMaxBlocks);
+    }
+    return stream_blocks(M);
 }
 
 int stream_blocks(int64_t M) {
@@ -84,6 +94,154 @@ __global__ void __launch_bounds__(kThreads) heisenberg_kernel(SpmvArgs a, int L,
             w = cfma_conj(ts, q, w);
         } else {
             w = cfma(rs, q, w);
+        }
+    }
+    if (a.part_w) {
+        __shared__ cplx scratch[kThreads / 32];
+        cplx v[1] = {w};
+        block_sum<1>(v, scratch);
+        if (threadIdx.x == 0) a.part_w[blockIdx.x] = v[0];
+    }
+}
+
+// Shared-memory tiled variant: a CTA stages a tile of 2^T consecutive states of r in shared
+// memory (one coalesced pass), applies the T-1 bonds inside the tile from shared memory, and
+// gathers only the L-T+1 bonds that leave the tile (bond (T-1,T), the tile-level bonds, and the
+// periodic bond (L-1,0)) from global memory — each a contiguous, coalesced 512-byte warp read
+// issued predicated and fully unrolled so that they are all in flight together.
+constexpr int kTileBits = kTileBitsPublic;
+
+template <int L, int T, int NRHS>
+__global__ void __launch_bounds__(kThreads, NRHS == 1 ? 4 : 2)
+heisenberg_tiled_kernel(SpmvArgs a, double J) {
+    // Bond-major within a tile of 2^T states.  Each thread owns PER = 2^T/256 states
+    // (ls = tid + 256 k) and keeps their q in registers.
+    //   round 1: own tile (-> shared memory + diagonal), bond (T-1,T) and the periodic bond
+    //            (L-1,0) — 3*PER independent loads in flight per thread;
+    //   rounds 2..: the ACTIVE tile-level bonds i >= T (a bond flips two tile-index bits, so the
+    //            whole tile takes part or none: the active set is uniform per CTA), three partner
+    //            tiles per round, each a coalesced stream;
+    //   then the T-1 bonds inside the tile from shared memory.
+    extern __shared__ cplx tile[];   // [NRHS][2^T]
+    using U = typename std::conditional<(L <= 31), uint32_t, uint64_t>::type;
+    int buf = 0;
+    if (a.st) {
+        if (a.st->status != ST_ITERATING) return;
+        buf = (int)(a.st->n_started % 3);
+    }
+    constexpr int TS = 1 << T;
+    constexpr int PER = TS / kThreads;
+    constexpr int NB = 3;   // tile-level bonds per round
+    static_assert(PER * kThreads == TS, "tile must be a multiple of the CTA size");
+    const cplx *__restrict__ r = pick3(a.r, buf);
+    const cplx *__restrict__ t = pick3(a.t, buf);
+    const double qJ = 0.25 * J, hJ = 0.5 * J;
+    const int64_t ntiles = a.M >> T;
+    const int tid = threadIdx.x;
+    cplx w = mk(0.0, 0.0);
+    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const U base = (U)(ti << T);
+        __syncthreads();   // previous tile's shared-memory reads are done
+        cplx q[PER], qt[NRHS == 2 ? PER : 1];
+        // ---- round 1 ---------------------------------------------------------------------
+        {
+            cplx v0[PER], v1[PER], v2[PER], t0[NRHS == 2 ? PER : 1], t1[NRHS == 2 ? PER : 1],
+                t2[NRHS == 2 ? PER : 1];
+            const U tb = (base >> T) & (U)1, hb = (base >> (L - 1)) & (U)1;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int ls = tid + k * kThreads;
+                const U s = base + (U)ls;
+                v0[k] = r[s];
+                if (NRHS == 2) t0[k] = t[s];
+                const bool on1 = ((U)((ls >> (T - 1)) & 1) ^ tb) != 0;    // bond (T-1, T)
+                const U s1 = s ^ ((U)3 << (T - 1));
+                v1[k] = on1 ? r[s1] : mk(0.0, 0.0);
+                if (NRHS == 2) t1[k] = on1 ? t[s1] : mk(0.0, 0.0);
+                const bool on2 = ((U)(ls & 1) ^ hb) != 0;                 // bond (L-1, 0)
+                const U s2 = s ^ (((U)1 << (L - 1)) | (U)1);
+                v2[k] = on2 ? r[s2] : mk(0.0, 0.0);
+                if (NRHS == 2) t2[k] = on2 ? t[s2] : mk(0.0, 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int ls = tid + k * kThreads;
+                const U s = base + (U)ls;
+                const U x = s ^ ((s >> 1) | ((s & (U)1) << (L - 1)));
+                const int na = (L <= 31) ? __popc((unsigned)x) : __popcll((unsigned long long)x);
+                const double d = qJ * (double)(L - 2 * na);
+                tile[ls] = v0[k];
+                q[k].x = fma(hJ, v1[k].x + v2[k].x, d * v0[k].x);
+                q[k].y = fma(hJ, v1[k].y + v2[k].y, d * v0[k].y);
+                if (NRHS == 2) {
+                    tile[TS + ls] = t0[k];
+                    qt[k].x = fma(hJ, t1[k].x + t2[k].x, d * t0[k].x);
+                    qt[k].y = fma(hJ, t1[k].y + t2[k].y, d * t0[k].y);
+                }
+            }
+        }
+        // ---- rounds 2..: active tile-level bonds (uniform per CTA) ----------------------------
+        if (L - 1 > T) {
+            const U tbits = base >> T;   // bit (i - T) of tbits = site i, for i >= T
+            U act = (tbits ^ (tbits >> 1)) & ((((U)1) << (L - 1 - T)) - (U)1);   // bonds T..L-2
+            while (act) {
+                int bi[NB];
+#pragma unroll
+                for (int m = 0; m < NB; ++m) {
+                    bi[m] = -1;
+                    if (act) {
+                        const int pos = (L <= 31) ? __ffs((int)act) - 1 : __ffsll((long long)act) - 1;
+                        bi[m] = pos + T;
+                        act &= act - (U)1;
+                    }
+                }
+                cplx v[NB][PER], vt[NB][NRHS == 2 ? PER : 1];
+#pragma unroll
+                for (int m = 0; m < NB; ++m) {
+                    const U pb = base ^ ((U)3 << (bi[m] < 0 ? 0 : bi[m]));
+#pragma unroll
+                    for (int k = 0; k < PER; ++k) {
+                        v[m][k] = bi[m] >= 0 ? r[pb + (U)(tid + k * kThreads)] : mk(0.0, 0.0);
+                        if (NRHS == 2) vt[m][k] = bi[m] >= 0 ? t[pb + (U)(tid + k * kThreads)] : mk(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < NB; ++m)
+#pragma unroll
+                    for (int k = 0; k < PER; ++k) {
+                        q[k].x = fma(hJ, v[m][k].x, q[k].x);
+                        q[k].y = fma(hJ, v[m][k].y, q[k].y);
+                        if (NRHS == 2) { qt[k].x = fma(hJ, vt[m][k].x, qt[k].x); qt[k].y = fma(hJ, vt[m][k].y, qt[k].y); }
+                    }
+            }
+        }
+        __syncthreads();   // tile staged
+        // ---- bonds inside the tile (i = 0 .. T-2) from shared memory -------------------------
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int ls = tid + k * kThreads;
+            const U s = base + (U)ls;
+            const U x = s ^ (s >> 1);   // bit i (< T-1): sites i, i+1 anti-aligned
+#pragma unroll
+            for (int i = 0; i < T - 1; ++i) {
+                if ((x >> i) & (U)1) {
+                    const cplx v = tile[ls ^ (3 << i)];
+                    q[k].x = fma(hJ, v.x, q[k].x);
+                    q[k].y = fma(hJ, v.y, q[k].y);
+                    if (NRHS == 2) {
+                        const cplx vt = tile[TS + (ls ^ (3 << i))];
+                        qt[k].x = fma(hJ, vt.x, qt[k].x);
+                        qt[k].y = fma(hJ, vt.y, qt[k].y);
+                    }
+                }
+            }
+            a.q[s] = q[k];
+            if (NRHS == 2) {
+                a.qt[s] = qt[k];
+                w = cfma_conj(tile[TS + ls], q[k], w);
+            } else {
+                w = cfma(tile[ls], q[k], w);
+            }
         }
     }
     if (a.part_w) {
@@ -161,7 +319,36 @@ csr_kernel(SpmvArgs a, const int64_t *__restrict__ rp, const int32_t *__restrict
     }
 }
 
+template <int L>
+static cudaError_t launch_tiled(const SpmvArgs &a, double J, int nblk, cudaStream_t s) {
+    constexpr int T = kTileBits;
+    const int grid = nblk;   // == heisenberg_blocks(L, M): one partial per CTA
+    const size_t shm = sizeof(cplx) << T;
+    if (a.bicg) {
+        static bool cfg = false;
+        if (!cfg) {
+            cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
+            cfg = true;
+        }
+        heisenberg_tiled_kernel<L, T, 2><<<grid, kThreads, 2 * shm, s>>>(a, J);
+    } else {
+        heisenberg_tiled_kernel<L, T, 1><<<grid, kThreads, shm, s>>>(a, J);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_heisenberg(const SpmvArgs &a, int L, double J, int nblk, cudaStream_t s) {
+    switch (L) {
+#define SK_TILED_CASE(LL) case LL: return launch_tiled<LL>(a, J, nblk, s);
+        SK_TILED_CASE(11) SK_TILED_CASE(12) SK_TILED_CASE(13) SK_TILED_CASE(14) SK_TILED_CASE(15) SK_TILED_CASE(16)
+        SK_TILED_CASE(17) SK_TILED_CASE(18) SK_TILED_CASE(19) SK_TILED_CASE(20) SK_TILED_CASE(21)
+        SK_TILED_CASE(22) SK_TILED_CASE(23) SK_TILED_CASE(24) SK_TILED_CASE(25) SK_TILED_CASE(26)
+        SK_TILED_CASE(27) SK_TILED_CASE(28) SK_TILED_CASE(29) SK_TILED_CASE(30) SK_TILED_CASE(31)
+        SK_TILED_CASE(32) SK_TILED_CASE(33) SK_TILED_CASE(34)
+#undef SK_TILED_CASE
+        default: break;
+    }
     if (a.bicg)
         heisenberg_kernel<2><<<nblk, kThreads, 0, s>>>(a, L, J);
     else
@@ -236,10 +423,12 @@ __global__ void __launch_bounds__(kThreads) init_kernel(KParams kp, const cplx *
 }
 
 // ============================================================================ fused update
-template <int NLMAX, bool BICG, bool FULL>
+// Each thread owns R rows per sweep (rows tid, tid+256, ... of a 256*R chunk) and issues all of
+// their loads before any arithmetic, so 4R+ independent 16-byte loads are in flight per thread.
+template <int NLMAX, bool BICG, bool FULL, int R>
 __global__ void __launch_bounds__(kThreads)
 update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
-    extern __shared__ cplx dyn[];  // FULL: coef[3 * nact], then act list (int32)
+    extern __shared__ cplx dyn[];  // FULL: coef[3 * nz], then act list (int32)
     DevState *st = kp.st;
     if (st->status != ST_ITERATING) return;
     const int64_t ns = st->n_started;            // start(n) ran: ns = n + 1
@@ -265,56 +454,72 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
 #pragma unroll
     for (int j = 0; j < 2 + NLMAX; ++j) acc[j] = mk(0.0, 0.0);
     const int64_t M = kp.M;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const cplx rc = ldg_cs(rc_ + i);
-        const cplx rp = ldg_cs(rp_ + i);
-        const cplx qi = ldg_cs(q + i);
-        cplx rn = cmul(a_cur, rc);
-        rn = cfma(a_q, qi, rn);
-        rn = cfma(a_prev, rp, rn);
-        rn_[i] = rn;
-        if (BICG) {
-            const cplx tc = ldg_cs(tc_ + i), tp = ldg_cs(tp_ + i), qti = ldg_cs(qt + i);
-            cplx tn = cmul(ac_cur, tc);
-            tn = cfma(ac_q, qti, tn);
-            tn = cfma(ac_prev, tp, tn);
-            tn_[i] = tn;
-            acc[0] = cfma_conj(tn, rn, acc[0]);
-        } else {
-            acc[0] = cfma(rn, rn, acc[0]);
-        }
-        acc[1].x = fma(rn.x, rn.x, fma(rn.y, rn.y, acc[1].x));
+    const int nl = kp.nl;
+    const int64_t chunk = (int64_t)kThreads * R;
+    for (int64_t base = (int64_t)blockIdx.x * chunk; base < M; base += (int64_t)gridDim.x * chunk) {
+        cplx rc[R], rp[R], qi[R], tc[R], tp[R], qti[R], lv[R][NLMAX];
 #pragma unroll
-        for (int l = 0; l < NLMAX; ++l)
-            if (l < kp.nl) acc[2 + l] = cfma_conj(ldg_cs(kp.left + (int64_t)l * M + i), rn, acc[2 + l]);
-        if (FULL) {
-            int j = 0;
-            for (; j + 4 <= nact; j += 4) {
-                cplx pk[4], xk[4];
+        for (int k = 0; k < R; ++k) {
+            const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
+            if (i < M) {
+                rc[k] = ldg_cs(rc_ + i);
+                rp[k] = ldg_cs(rp_ + i);
+                qi[k] = ldg_cs(q + i);
+                if (BICG) { tc[k] = ldg_cs(tc_ + i); tp[k] = ldg_cs(tp_ + i); qti[k] = ldg_cs(qt + i); }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t off = (int64_t)act[j + u] * M + i;
-                    pk[u] = ldg_cs(kp.p + off);
-                    xk[u] = ldg_cs(kp.x + off);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t off = (int64_t)act[j + u] * M + i;
-                    cplx pn = cmul(coef[3 * (j + u)], rc);
-                    pn = cfma(coef[3 * (j + u) + 1], pk[u], pn);
-                    const cplx xn = cfma(coef[3 * (j + u) + 2], pn, xk[u]);
-                    stg_cs(kp.p + off, pn);
-                    stg_cs(kp.x + off, xn);
-                }
+                for (int l = 0; l < NLMAX; ++l)
+                    if (l < nl) lv[k][l] = ldg_cs(kp.left + (int64_t)l * M + i);
             }
-            for (; j < nact; ++j) {
-                const int64_t off = (int64_t)act[j] * M + i;
-                const cplx pk = ldg_cs(kp.p + off), xk = ldg_cs(kp.x + off);
-                cplx pn = cmul(coef[3 * j], rc);
-                pn = cfma(coef[3 * j + 1], pk, pn);
-                stg_cs(kp.p + off, pn);
-                stg_cs(kp.x + off, cfma(coef[3 * j + 2], pn, xk));
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
+            if (i >= M) continue;
+            cplx rn = cmul(a_cur, rc[k]);
+            rn = cfma(a_q, qi[k], rn);
+            rn = cfma(a_prev, rp[k], rn);
+            rn_[i] = rn;
+            if (BICG) {
+                cplx tn = cmul(ac_cur, tc[k]);
+                tn = cfma(ac_q, qti[k], tn);
+                tn = cfma(ac_prev, tp[k], tn);
+                tn_[i] = tn;
+                acc[0] = cfma_conj(tn, rn, acc[0]);
+            } else {
+                acc[0] = cfma(rn, rn, acc[0]);
+            }
+            acc[1].x = fma(rn.x, rn.x, fma(rn.y, rn.y, acc[1].x));
+#pragma unroll
+            for (int l = 0; l < NLMAX; ++l)
+                if (l < nl) acc[2 + l] = cfma_conj(lv[k][l], rn, acc[2 + l]);
+            if (FULL) {
+                const cplx r0 = rc[k];
+                int j = 0;
+                for (; j + 4 <= nact; j += 4) {
+                    cplx pk[4], xk[4];
+#pragma unroll
+                    for (int uu = 0; uu < 4; ++uu) {
+                        const int64_t off = (int64_t)act[j + uu] * M + i;
+                        pk[uu] = ldg_cs(kp.p + off);
+                        xk[uu] = ldg_cs(kp.x + off);
+                    }
+#pragma unroll
+                    for (int uu = 0; uu < 4; ++uu) {
+                        const int64_t off = (int64_t)act[j + uu] * M + i;
+                        cplx pn = cmul(coef[3 * (j + uu)], r0);
+                        pn = cfma(coef[3 * (j + uu) + 1], pk[uu], pn);
+                        stg_cs(kp.p + off, pn);
+                        stg_cs(kp.x + off, cfma(coef[3 * (j + uu) + 2], pn, xk[uu]));
+                    }
+                }
+                for (; j < nact; ++j) {
+                    const int64_t off = (int64_t)act[j] * M + i;
+                    const cplx pk = ldg_cs(kp.p + off), xk = ldg_cs(kp.x + off);
+                    cplx pn = cmul(coef[3 * j], r0);
+                    pn = cfma(coef[3 * j + 1], pk, pn);
+                    stg_cs(kp.p + off, pn);
+                    stg_cs(kp.x + off, cfma(coef[3 * j + 2], pn, xk));
+                }
             }
         }
     }
@@ -327,24 +532,26 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
     }
 }
 
+template <int NLMAX, bool BICG, bool FULL>
+static cudaError_t launch_update_t(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
+    constexpr int R = FULL ? 1 : (NLMAX <= 4 ? 4 : (NLMAX <= 8 ? 2 : 1));
+    const size_t shm = FULL ? (size_t)kp.nz * (3 * sizeof(cplx) + sizeof(int)) : 0;
+    if (FULL && shm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(update_kernel<NLMAX, BICG, FULL, R>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (e != cudaSuccess) return e;
+    }
+    update_kernel<NLMAX, BICG, FULL, R><<<kp.nblk_upd, kThreads, shm, s>>>(kp, q, qt);
+    return cudaGetLastError();
+}
+
 template <int NLMAX>
 static cudaError_t launch_update_nl(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
-    const size_t shm = kp.full ? (size_t)kp.nz * (3 * sizeof(cplx) + sizeof(int)) : 0;
-    if (kp.full) {
-        if (kp.bicg) {
-            cudaFuncSetAttribute(update_kernel<NLMAX, true, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-            update_kernel<NLMAX, true, true><<<kp.nblk_upd, kThreads, shm, s>>>(kp, q, qt);
-        } else {
-            cudaFuncSetAttribute(update_kernel<NLMAX, false, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-            update_kernel<NLMAX, false, true><<<kp.nblk_upd, kThreads, shm, s>>>(kp, q, qt);
-        }
-    } else {
-        if (kp.bicg) update_kernel<NLMAX, true, false><<<kp.nblk_upd, kThreads, 0, s>>>(kp, q, qt);
-        else update_kernel<NLMAX, false, false><<<kp.nblk_upd, kThreads, 0, s>>>(kp, q, qt);
-    }
-    return cudaGetLastError();
+    if (kp.full)
+        return kp.bicg ? launch_update_t<NLMAX, true, true>(kp, q, qt, s)
+                       : launch_update_t<NLMAX, false, true>(kp, q, qt, s);
+    return kp.bicg ? launch_update_t<NLMAX, true, false>(kp, q, qt, s)
+                   : launch_update_t<NLMAX, false, false>(kp, q, qt, s);
 }
 
 cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
@@ -361,277 +568,6 @@ cudaError_t launch_init(const KParams &kp, const cplx *b, cudaStream_t s) {
     else if (kp.nl <= 8) init_kernel<8><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
     else if (kp.nl <= 16) init_kernel<16><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
     else init_kernel<32><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
-    return cudaGetLastError();
-}
-
-// ============================================================================ scalar kernel
-// One CTA of kScalarThreads threads.  Shared broadcast slots + deterministic block reductions.
-struct ScalarShared {
-    cplx red[kScalarThreads / 32 + 1];
-    double redd[kScalarThreads / 32];
-    int redi[kScalarThreads / 32];
-    cplx g[64];
-    cplx bc[8];      // broadcast scalars
-    int bci[4];
-};
-
-__device__ cplx block_allsum(cplx v, ScalarShared &sh) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v = warp_sum(v);
-    if (lane == 0) sh.red[warp] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cplx s = sh.red[0];
-        for (int w = 1; w < nw; ++w) s = cadd(s, sh.red[w]);
-        sh.red[32] = s;
-    }
-    __syncthreads();
-    const cplx r = sh.red[32];
-    __syncthreads();
-    return r;
-}
-
-__device__ int block_allsum_int(int v, ScalarShared &sh) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) sh.redi[warp] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int w = 0; w < nw; ++w) s += sh.redi[w];
-        sh.bci[3] = s;
-    }
-    __syncthreads();
-    const int r = sh.bci[3];
-    __syncthreads();
-    return r;
-}
-
-// Sum partial column j of part[nblk][stride] in fixed order -> broadcast.
-__device__ cplx reduce_partials(const cplx *part, int nblk, int stride, int j, ScalarShared &sh) {
-    cplx v = mk(0.0, 0.0);
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) v = cadd(v, part[(int64_t)b * stride + j]);
-    return block_allsum(v, sh);
-}
-
-// argmin over active shifts of |pi_k|, ties -> lowest k; returns -1 if none active.
-__device__ int block_argmin_active(const KParams &kp, ScalarShared &sh) {
-    double best = 0.0;
-    int bi = -1;
-    for (int k = threadIdx.x; k < kp.nz; k += blockDim.x) {
-        if (!kp.active[k]) continue;
-        const double v = cabsd(kp.pi[k]);
-        if (bi < 0 || v < best) { best = v; bi = k; }
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (oi >= 0 && (bi < 0 || ov < best || (ov == best && oi < bi))) { best = ov; bi = oi; }
-    }
-    if (lane == 0) { sh.redd[warp] = best; sh.redi[warp] = bi; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double b = 0.0; int i = -1;
-        for (int w = 0; w < nw; ++w) {
-            const int oi = sh.redi[w]; const double ov = sh.redd[w];
-            if (oi >= 0 && (i < 0 || ov < b || (ov == b && oi < i))) { b = ov; i = oi; }
-        }
-        sh.bci[2] = i;
-    }
-    __syncthreads();
-    const int r = sh.bci[2];
-    __syncthreads();
-    return r;
-}
-
-__global__ void __launch_bounds__(kScalarThreads) scalar_kernel(KParams kp, int phases) {
-    __shared__ ScalarShared sh;
-    DevState *st = kp.st;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int nred = 2 + kp.nl;
-
-    if (phases & PH_INIT) {
-        const cplx rho = reduce_partials(kp.part_u, kp.nblk_upd, nred, 0, sh);
-        const double nu = sqrt(reduce_partials(kp.part_u, kp.nblk_upd, nred, 1, sh).x);
-        for (int l = 0; l < kp.nl; ++l) {
-            const cplx g = reduce_partials(kp.part_u, kp.nblk_upd, nred, 2 + l, sh);
-            if (tid == 0) kp.g[l] = g;
-        }
-        for (int k = tid; k < kp.nz; k += nt) kp.res[k] = nu;
-        if (tid == 0) { st->rho_cur = rho; st->nu = nu; }
-        return;
-    }
-
-    const int pending = st->pending;
-    __syncthreads();
-    if ((phases & PH_FINISH) && pending) {
-        // --- a8: residuals of r_{n+1} (stored unscaled), retirement ------------------------
-        cplx rho = reduce_partials(kp.part_u, kp.nblk_upd, nred, 0, sh);
-        double nu = sqrt(reduce_partials(kp.part_u, kp.nblk_upd, nred, 1, sh).x);
-        for (int l = 0; l < kp.nl; ++l) {
-            const cplx g = reduce_partials(kp.part_u, kp.nblk_upd, nred, 2 + l, sh);
-            if (tid == 0) sh.g[l] = g;
-        }
-        const int64_t n = st->n + 1;
-        const double tol = st->tol;
-        int cnt = 0;
-        for (int k = tid; k < kp.nz; k += nt) {
-            if (!kp.active[k]) continue;
-            const double res = nu / cabsd(kp.pi[k]);
-            kp.res[k] = res;
-            if (res < tol) { kp.active[k] = 0; kp.retired_at[k] = n; }
-            else ++cnt;
-        }
-        __syncthreads();
-        cnt = block_allsum_int(cnt, sh);
-        // --- a9: seed switching --------------------------------------------------------------
-        int best = -1;
-        if (cnt > 0) best = block_argmin_active(kp, sh);
-        const int doswitch = cnt > 0 && !(kp.flags & 1) && best != st->seed;
-        cplx f = mk(1.0, 0.0), fp = mk(1.0, 0.0);
-        if (doswitch) {
-            f = kp.pi[best];
-            fp = kp.pi_old[best];
-            __syncthreads();   // everyone read pi[best] before it is rescaled
-            const cplx rf = crecip(f), rfp = crecip(fp);
-            for (int k = tid; k < kp.nz; k += nt) {
-                if (!kp.active[k]) continue;
-                kp.pi[k] = cmul(kp.pi[k], rf);
-                kp.pi_old[k] = cmul(kp.pi_old[k], rfp);
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
-            if (doswitch) {   // DESIGN.md R9: the new seed's r, r_prev, pi, alpha, rho
-                st->sr_cur = cdiv(st->sr_cur, f);                          // r_{n+1} /= f
-                st->sr_prev = cdiv(st->sr_prev, fp);                       // r_n /= f'
-                st->alpha_prev = cmul(st->alpha_prev, cdiv(fp, f));        // alpha_n^{s*}
-                st->rho_prev = cdiv(st->rho_prev, cmul(fp, fp));           // rho_n / f'^2
-                rho = cdiv(rho, cmul(f, f));                               // rho_{n+1} / f^2
-                nu = nu / cabsd(f);
-                for (int l = 0; l < kp.nl; ++l) sh.g[l] = cdiv(sh.g[l], f);
-                st->zs = kp.z[best];
-                st->seed = best;
-                st->nswitch += 1;
-            }
-            st->rho_cur = rho;
-            st->nu = nu;
-            for (int l = 0; l < kp.nl; ++l) kp.g[l] = sh.g[l];
-            st->n = n;
-            st->pending = 0;
-            st->n_active = cnt;
-            if (cnt == 0) st->status = ST_CONVERGED;
-            else if (n >= st->itermax) st->status = ST_MAXITER;
-        }
-        __syncthreads();
-    }
-
-    if (!(phases & PH_START)) return;
-    if (st->status != ST_ITERATING) return;   // uniform: written before the last barrier
-
-    // --- a3: seed scalars ---------------------------------------------------------------------
-    const cplx wraw = reduce_partials(kp.part_w, kp.nblk_spmv, 1, 0, sh);
-    if (tid == 0) {
-        const cplx sr = st->sr_cur;
-        const cplx w = cmul(cmul(sr, sr), wraw);   // w_n = <r~_n|r_n, H r_n> (true scale)
-        const cplx rho = st->rho_cur;
-        const int64_t n = st->n;
-        cplx beta = mk(0, 0), gamma = mk(0, 0);
-        if (n > 0) {
-            beta = cdiv(rho, st->rho_prev);           // EQ-REC-BETA P:L262
-            gamma = cdiv(beta, st->alpha_prev);
-        }
-        // EQ-REC-ALPHA-N2: alpha = rho / (<r, A r> - gamma rho), <r, A r> = z_s rho - w
-        const cplx den = csub(csub(cmul(st->zs, rho), w), cmul(gamma, rho));
-        int brk = (cabsd(rho) < 1e-300) || (cabsd(den) < 1e-300);
-        cplx alpha = mk(0, 0), c = mk(0, 0);
-        if (!brk) {
-            alpha = cdiv(rho, den);
-            c = cmul(alpha, gamma);
-        }
-        sh.bc[0] = alpha; sh.bc[1] = beta; sh.bc[2] = c;
-        sh.bci[0] = brk;
-        st->alpha = alpha; st->beta = beta; st->w = w;
-        if (brk) st->status = ST_BREAKDOWN;
-    }
-    __syncthreads();
-    if (sh.bci[0]) return;
-    const cplx alpha = sh.bc[0], beta = sh.bc[1], c = sh.bc[2];
-    const cplx zs = st->zs, sr = st->sr_cur;
-    const int64_t n = st->n;
-    const int nl = kp.nl;
-
-    // compacted active list (ascending shift order): the full-mode kernel streams only these
-    int nact = 0;
-    {
-        const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-        for (int base = 0; base < kp.nz; base += nt) {
-            const int k = base + tid;
-            const int a = (k < kp.nz) ? (int)kp.active[k] : 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, a);
-            const int wpre = __popc(bal & ((1u << lane) - 1u));
-            if (lane == 0) sh.redi[warp] = __popc(bal);
-            __syncthreads();
-            if (tid == 0) {
-                int acc = 0;
-                for (int w = 0; w < nw; ++w) { const int v = sh.redi[w]; sh.redi[w] = acc; acc += v; }
-                sh.bci[1] = acc;
-            }
-            __syncthreads();
-            if (a) kp.act_list[nact + sh.redi[warp] + wpre] = k;
-            nact += sh.bci[1];
-            __syncthreads();
-        }
-        if (tid == 0) *kp.n_act_list = nact;
-    }
-    __syncthreads();
-
-    // --- a4 + a6 + (a7 coefficients): per-shift recurrences -------------------------------------
-    const cplx one = mk(1.0, 0.0);
-    for (int j = tid; j < nact; j += nt) {
-        const int k = kp.act_list[j];
-        const cplx pik = kp.pi[k], pio = kp.pi_old[k];
-        const cplx sigma = csub(kp.z[k], zs);
-        // EQ-SHIFTEDCG-PI: pi_{n+1} = (1 + c + alpha sigma) pi_n - c pi_{n-1}
-        const cplx pin = csub(cmul(cadd(cadd(one, c), cmul(alpha, sigma)), pik), cmul(c, pio));
-        const cplx ak = cmul(cdiv(pik, pin), alpha);
-        cplx bk = mk(0, 0);
-        if (n > 0) { const cplx rat = cdiv(pio, pik); bk = cmul(cmul(rat, rat), beta); }
-        for (int l = 0; l < nl; ++l) {                                           // P:L372-376 (R1)
-            const int64_t o = (int64_t)k * nl + l;
-            const cplx u = cadd(cdiv(kp.g[l], pik), cmul(bk, kp.u[o]));
-            kp.u[o] = u;
-            kp.y[o] = cfma(ak, u, kp.y[o]);
-        }
-        kp.pi_old[k] = pik;
-        kp.pi[k] = pin;
-        if (kp.full) {
-            kp.coef[3 * j] = cdiv(sr, pik);    // p^k = r_n/pi_n^k + ...   (r_n = sr * r_stored)
-            kp.coef[3 * j + 1] = bk;
-            kp.coef[3 * j + 2] = ak;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        // update coefficients (a5) in stored-vector form, then rotate the lazy scales
-        st->a_cur = cmul(csub(cadd(one, c), cmul(alpha, zs)), sr);
-        st->a_q = cmul(alpha, sr);
-        st->a_prev = cmul(mk(-c.x, -c.y), st->sr_prev);
-        st->sr_prev = sr;
-        st->sr_cur = one;
-        st->alpha_prev = alpha;
-        st->rho_prev = st->rho_cur;
-        st->n_started = n + 1;
-        st->pending = 1;
-        st->nspmv += kp.bicg ? 2 : 1;
-    }
-}
-
-cudaError_t launch_scalar(const KParams &kp, int phases, cudaStream_t s) {
-    scalar_kernel<<<1, kScalarThreads, 0, s>>>(kp, phases);
     return cudaGetLastError();
 }
 

@@ -11,7 +11,9 @@ constexpr int kMaxBlocks = 148 * 8;    // grid cap for grid-stride streaming ker
 // Scalar-kernel phases.
 enum : int { PH_INIT = 1, PH_FINISH = 2, PH_START = 4 };
 
+constexpr int kTileBitsPublic = 10;  // Heisenberg tile: 2^10 states per CTA
 int stream_blocks(int64_t M);
+int heisenberg_blocks(int L, int64_t M);   // grid (and partial count) of the Heisenberg SpMV
 
 // SpMV q = H r (and qt = H t for BiCG) with the fused partial dot w = <tv, q>.
 // When `st` is null the kernel runs standalone on r0/t0 (sk_apply_operator) without partials.

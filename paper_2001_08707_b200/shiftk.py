@@ -28,7 +28,7 @@ ERRORS = {0: "SK_OK", -1: "SK_EINVAL", -2: "SK_ENOMEM", -3: "SK_ECUDA", -4: "SK_
 EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_run", "sk_enqueue",
            "sk_get_residual", "sk_get_projection", "sk_get_solution", "sk_get_shift_state",
            "sk_get_coefficients", "sk_finalize", "sk_apply_operator", "sk_last_error", "sk_version",
-           "sk_profile_enable", "sk_get_profile", "sk_copy_solution"]
+           "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps"]
 
 
 class ShiftkError(RuntimeError):
@@ -102,6 +102,7 @@ def load(path: str = LIB_PATH):
         "sk_apply_operator": [P(sk_operator), VP, VP, VP],
         "sk_profile_enable": [VP, I32],
         "sk_copy_solution": [VP, I64, VP, I32],
+        "sk_debug_timestamps": [VP, VP],
         "sk_get_profile": [VP, P(sk_profile), I32],
     }
     for name, args in sig.items():
@@ -274,6 +275,11 @@ class Solver:
                     spmv_count=c.spmv_count, n_active=c.n_active, status=c.status,
                     z_seed=cz(c.z_seed), alpha=cz(c.alpha), rho=cz(c.rho), beta=cz(c.beta),
                     seed_residual=c.seed_residual)
+
+    def debug_timestamps(self) -> np.ndarray:
+        out = np.zeros(16, dtype=np.int64)
+        _check(load().sk_debug_timestamps(self._h, out.ctypes.data), "sk_debug_timestamps")
+        return out
 
     def profile_enable(self, on: bool = True):
         _check(load().sk_profile_enable(self._h, int(on)), "sk_profile_enable")
