@@ -211,18 +211,19 @@ const char *sk_last_error(void);
 typedef struct {
     int64_t iterations;      /* iterations timed since the last reset                          */
     int64_t launches;        /* kernels this library launched since sk_init (all modes)        */
-    double ms_spmv;          /* summed device time of the SpMV (+ fused w) kernels             */
-    double ms_scalar;        /* summed device time of the scalar (recurrence) kernels          */
-    double ms_update;        /* summed device time of the fused update kernels                 */
+    double ms_spmv;          /* summed device time of the SpMV kernels (+ fused w, the finish of
+                                the previous iteration and the seed scalars)                    */
+    double ms_scalar;        /* summed device time of stand-alone scalar kernels (0 in a loop) */
+    double ms_update;        /* summed device time of the fused update kernels (+ per-shift
+                                recurrences)                                                    */
 } sk_profile;
 
 int sk_profile_enable(sk_ctx *ctx, int32_t on);
 /* Synchronises the stream, accumulates the recorded events into *out; reset != 0 clears. */
 int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
 
-/* Diagnostics: %globaltimer stamps (ns) written by the last scalar-step kernel at its phase
-   boundaries [0 entry, 1 inputs staged, 2 finish done, 5 seed scalars, 6 compaction,
-   3 start done, 4 exit].  Requires the environment variable SHIFTK_DEBUG_TS at sk_init. */
+/* Diagnostics: %globaltimer stamps (ns) written by instrumented kernels (16 slots; see
+   csrc/steps.cuh).  Requires the environment variable SHIFTK_DEBUG_TS at sk_init. */
 int sk_debug_timestamps(sk_ctx *ctx, int64_t *out16);
 
 /* Library version / build info string (never NULL). */

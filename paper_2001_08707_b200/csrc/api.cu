@@ -14,6 +14,7 @@
 #include "../../include/shiftk.h"
 #include "kernels.cuh"
 
+
 static thread_local std::string g_err = "no error";
 
 static int fail(int code, const std::string &msg) {
@@ -95,40 +96,30 @@ static void destroy(sk_ctx *c) {
 }
 
 // --------------------------------------------------------------------------- enqueue helpers
-static int enqueue_spmv(sk_ctx *c) {
+// One iteration = two launches:
+//   SpMV (+ finish of the previous iteration in CTA 0, + seed scalars in the last CTA)
+//   update (+ per-shift recurrences in CTA 0).
+static int enqueue_iteration(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc) {
     sk::SpmvArgs a{};
     a.st = c->st;
     for (int i = 0; i < 3; ++i) { a.r[i] = c->kp.r[i]; a.t[i] = c->kp.t[i]; }
-    a.q = c->kp.q;
-    a.qt = c->kp.qt;
+    a.q = q_rc ? (cplx *)q_rc : c->kp.q;
+    a.qt = q_rc ? (cplx *)qt_rc : c->kp.qt;
     a.part_w = c->kp.part_w;
     a.M = c->M;
     a.bicg = c->method == SK_BICG;
-    cudaError_t e;
-    if (c->op.kind == SK_OP_HEISENBERG)
-        e = sk::launch_heisenberg(a, c->op.L, c->op.J, c->kp.nblk_spmv, c->stream);
+    CK(prof_mark(c));
+    if (q_rc)
+        CK(sk::launch_rc_dot(a, c->kp, c->stream));
+    else if (c->op.kind == SK_OP_HEISENBERG)
+        CK(sk::launch_heisenberg(a, c->kp, c->op.L, c->op.J, c->stream));
     else
-        e = sk::launch_csr(a, c->op.row_ptr, c->op.col, c->op.val, c->op.kind == SK_OP_CSR_CPLX,
-                           c->avg_nnz, c->kp.nblk_spmv, c->stream);
-    CK(e);
-    return SK_OK;
-}
-
-// One iteration: [SpMV] -> scalar(finish previous + start) -> fused update.
-static int enqueue_iteration(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc) {
-    int rc;
+        CK(sk::launch_csr(a, c->kp, c->op.row_ptr, c->op.col, c->op.val, c->op.kind == SK_OP_CSR_CPLX,
+                          c->avg_nnz, c->stream));
     CK(prof_mark(c));
-    if (q_rc) {
-        CK(sk::launch_rc_dot(c->kp, q_rc, c->stream));
-    } else if ((rc = enqueue_spmv(c)) != SK_OK) {
-        return rc;
-    }
+    CK(sk::launch_update(c->kp, a.q, a.qt, c->stream));
     CK(prof_mark(c));
-    CK(sk::launch_scalar(c->kp, sk::PH_FINISH | sk::PH_START, c->stream));
-    CK(prof_mark(c));
-    CK(sk::launch_update(c->kp, q_rc ? q_rc : c->kp.q, q_rc ? qt_rc : c->kp.qt, c->stream));
-    CK(prof_mark(c));
-    if (!c->capturing) c->launches += 3;
+    if (!c->capturing) c->launches += 2;
     c->host_started += 1;
     c->pending_host = true;
     return SK_OK;
@@ -231,7 +222,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
     kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M) : sk::stream_blocks(M);
-    kp.nblk_upd = sk::stream_blocks(M);
+    kp.nblk_upd = sk::update_blocks(M, c->nl, c->full);
     const size_t vb = (size_t)M * sizeof(cplx);
 
     // One device arena for everything the context owns (one cudaMalloc / cudaFree); every
@@ -253,17 +244,17 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&kp.part_w, sizeof(cplx) * sk::kMaxBlocks);
         add(&kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
         add(&zdev, sizeof(cplx) * c->nz);
-        add(&kp.pi, sizeof(cplx) * c->nz);
-        add(&kp.pi_old, sizeof(cplx) * c->nz);
+        add(&kp.pibuf, sizeof(cplx) * 3 * c->nz);
+        add(&kp.pi_frozen, sizeof(cplx) * c->nz);
+        add(&kp.ticket, sizeof(uint32_t));
         add(&kp.active, c->nz);
         add(&kp.res, sizeof(double) * c->nz);
         add(&kp.retired_at, sizeof(int64_t) * c->nz);
         add(&kp.u, sizeof(cplx) * c->nz * c->nl);
         add(&kp.y, sizeof(cplx) * c->nz * c->nl);
         add(&kp.g, sizeof(cplx) * c->nl);
-        add(&kp.coef, sizeof(cplx) * 3 * c->nz);
         add(&kp.act_list, sizeof(int32_t) * c->nz);
-        add(&kp.n_act_list, sizeof(int32_t));
+        add(&kp.n_act, sizeof(int32_t));
         if (getenv("SHIFTK_DEBUG_TS")) add(&kp.dbg_ts, sizeof(int64_t) * 16);
         if (!c->a_is_b && p->left_mem != SK_MEM_DEVICE) add(&c->left_owned, vb * c->nl);
         if (c->full) {
@@ -299,11 +290,10 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     }
     // per-shift init: pi_0 = pi_{-1} = 1, active, retired_at = -1
     {
-        std::vector<cplx> ones(c->nz, mk(1.0, 0.0));
+        std::vector<cplx> ones(3 * (size_t)c->nz, mk(1.0, 0.0));   // pi_0 = pi_{-1} = 1
         std::vector<uint8_t> act(c->nz, 1);
         std::vector<int64_t> ret(c->nz, -1);
-        if (cudaMemcpyAsync(kp.pi, ones.data(), sizeof(cplx) * c->nz, cudaMemcpyHostToDevice, c->stream) ||
-            cudaMemcpyAsync(kp.pi_old, ones.data(), sizeof(cplx) * c->nz, cudaMemcpyHostToDevice, c->stream) ||
+        if (cudaMemcpyAsync(kp.pibuf, ones.data(), sizeof(cplx) * 3 * c->nz, cudaMemcpyHostToDevice, c->stream) ||
             cudaMemcpyAsync(kp.active, act.data(), c->nz, cudaMemcpyHostToDevice, c->stream) ||
             cudaMemcpyAsync(kp.retired_at, ret.data(), sizeof(int64_t) * c->nz, cudaMemcpyHostToDevice, c->stream))
             return bail(fail(SK_ECUDA, "init per-shift arrays"));
@@ -488,11 +478,23 @@ int sk_get_shift_state(sk_ctx *c, sk_cplx *pi, uint8_t *active, int64_t *retired
     if (!c) return fail(SK_ESTATE, "null context");
     int rc;
     if ((rc = enqueue_finish(c)) != SK_OK) return rc;
-    if (pi) CK(cudaMemcpyAsync(pi, c->kp.pi, sizeof(cplx) * c->nz, cudaMemcpyDeviceToHost, c->stream));
-    if (active) CK(cudaMemcpyAsync(active, c->kp.active, c->nz, cudaMemcpyDeviceToHost, c->stream));
-    if (retired_at)
-        CK(cudaMemcpyAsync(retired_at, c->kp.retired_at, sizeof(int64_t) * c->nz, cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    const int64_t n = c->st_host->n;
+    std::vector<cplx> cur(c->nz), frozen(c->nz);
+    std::vector<uint8_t> act(c->nz);
+    std::vector<int64_t> ret(c->nz);
+    CK(cudaMemcpyAsync(cur.data(), c->kp.pibuf + (size_t)(n % 3) * c->nz, sizeof(cplx) * c->nz,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(frozen.data(), c->kp.pi_frozen, sizeof(cplx) * c->nz, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(act.data(), c->kp.active, c->nz, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(ret.data(), c->kp.retired_at, sizeof(int64_t) * c->nz, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < c->nz; ++k) {
+        const cplx v = act[k] ? cur[k] : frozen[k];   // retired shifts report pi at retirement
+        if (pi) pi[k] = {v.x, v.y};
+        if (active) active[k] = act[k];
+        if (retired_at) retired_at[k] = ret[k];
+    }
     return SK_OK;
 }
 
@@ -526,14 +528,14 @@ int sk_profile_enable(sk_ctx *c, int32_t on) {
 int sk_get_profile(sk_ctx *c, sk_profile *o, int32_t reset) {
     if (!c || !o) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
     CK(cudaStreamSynchronize(c->stream));
-    // events come in groups of 4 per iteration: [spmv] [scalar] [update]
-    const size_t groups = c->ev_used / 4;
+    // events come in groups of 3 per iteration: [spmv (+finish, +seed)] [update (+shift step)]
+    const size_t groups = c->ev_used / 3;
     for (size_t i = 0; i < groups; ++i) {
-        for (int k = 0; k < 3; ++k) {
-            float ms = 0;
-            CK(cudaEventElapsedTime(&ms, c->ev_pool[4 * i + k], c->ev_pool[4 * i + k + 1]));
-            c->prof_ms[k] += ms;
-        }
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->ev_pool[3 * i], c->ev_pool[3 * i + 1]));
+        c->prof_ms[0] += ms;
+        CK(cudaEventElapsedTime(&ms, c->ev_pool[3 * i + 1], c->ev_pool[3 * i + 2]));
+        c->prof_ms[2] += ms;
     }
     c->prof_iters += (int64_t)groups;
     c->ev_used = 0;
@@ -576,13 +578,13 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
     if (H->kind == SK_OP_HEISENBERG) {
         if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L)) return fail(SK_EINVAL, "L/M");
         a.M = H->M;
-        CK(sk::launch_heisenberg(a, H->L, H->J, sk::heisenberg_blocks(H->L, a.M), s));
+        CK(sk::launch_heisenberg(a, KParams{}, H->L, H->J, s));
     } else if (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) {
         const int64_t M = H->M_local > 0 ? H->M_local : H->M;
         if (!H->row_ptr || !H->col || !H->val || M < 1) return fail(SK_EINVAL, "CSR");
         a.M = M;
-        CK(sk::launch_csr(a, H->row_ptr, H->col, H->val, H->kind == SK_OP_CSR_CPLX,
-                          double(H->nnz) / double(M), sk::stream_blocks(M), s));
+        CK(sk::launch_csr(a, KParams{}, H->row_ptr, H->col, H->val, H->kind == SK_OP_CSR_CPLX,
+                          double(H->nnz) / double(M), s));
     } else {
         return fail(SK_EINVAL, "operator kind");
     }

@@ -14,33 +14,19 @@ __host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
     return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __host__ __device__ __forceinline__ cplx cconj(cplx a) { return mk(a.x, -a.y); }
-__host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return mk(a.x * s, a.y * s); }
 __host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
-__host__ __device__ __forceinline__ double cabsd(cplx a) { return hypot(a.x, a.y); }
-// a * conj-free fused: acc += a * b
+// acc + a * b
 __host__ __device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx acc) {
     return mk(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
 }
-// acc += conj(a) * b
+// acc + conj(a) * b
 __host__ __device__ __forceinline__ cplx cfma_conj(cplx a, cplx b, cplx acc) {
     return mk(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y)));
 }
-// Smith's algorithm: a / b without needless overflow/underflow.
-__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
-    if (fabs(b.x) >= fabs(b.y)) {
-        double r = b.y / b.x, d = b.x + b.y * r;
-        return mk((a.x + a.y * r) / d, (a.y - a.x * r) / d);
-    } else {
-        double r = b.x / b.y, d = b.x * r + b.y;
-        return mk((a.x * r + a.y) / d, (a.y * r - a.x) / d);
-    }
-}
-__host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(mk(1.0, 0.0), b); }
 
-__device__ __forceinline__ cplx ldg_cs(const cplx *p) {  // streaming load (read once)
-    return __ldcs(p);
-}
+__device__ __forceinline__ cplx ldg_cs(const cplx *p) { return __ldcs(p); }   // read once
 __device__ __forceinline__ void stg_cs(cplx *p, cplx v) { __stcs(p, v); }
+__device__ __forceinline__ cplx ldcg(const cplx *p) { return __ldcg(p); }     // L2 (coherent)
 
 __device__ __forceinline__ void dbg_stamp(int64_t *ts, int i) {
     if (ts && threadIdx.x == 0) {
@@ -82,17 +68,27 @@ __device__ __forceinline__ void block_sum(cplx (&v)[NV], cplx *scratch) {
     __syncthreads();
 }
 
+// select one of three by-value pointers without dynamic indexing (keeps them in registers)
+template <typename T>
+__host__ __device__ __forceinline__ T pick3(T const (&a)[3], int64_t i) {
+    const int k = (int)(i % 3);
+    return k == 0 ? a[0] : (k == 1 ? a[1] : a[2]);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Device-resident solver state (one per context).  Everything a kernel needs per iteration is
 // read from here, so a captured CUDA graph can replay iterations without host involvement.
+//
+// Iteration bookkeeping: `n` completed iterations.  r_n lives in r[n % 3] (stored form,
+// r_true = sr_cur * r_stored); pi_n^k in pibuf[n % 3][k], pi_{n-1} in pibuf[(n + 2) % 3].
 // ---------------------------------------------------------------------------------------------
 struct DevState {
     int64_t n;           // completed iterations
-    int64_t n_started;   // iterations whose seed/shift scalar step ran (buffer rotation index)
+    int64_t n_started;   // iterations whose seed scalars were computed
     int64_t nswitch;
     int64_t nspmv;
     int32_t status;      // sk_status
-    int32_t pending;     // 1: update(n) ran, finish(n) not yet
+    int32_t pending;     // 1: iteration n was updated, its finish (residuals/switch) not yet run
     int32_t seed;        // current seed index s
     int32_t n_active;
     cplx zs;             // seed shift z_s
@@ -101,11 +97,12 @@ struct DevState {
     cplx rho_prev;       // rho_{n-1}
     cplx sr_cur, sr_prev;   // lazy scale: r_true = sr * r_stored (shadow: conj(sr))
     cplx a_cur, a_q, a_prev; // r_{n+1} = a_cur r_cur_st + a_q q_raw + a_prev r_prev_st
+    cplx alpha, beta, c; // seed scalars of the current iteration (read by the shift step)
+    cplx sr_it;          // sr_cur used by the current iteration (full-mode coefficient)
+    cplx w;              // diagnostics
     double nu;           // ||r_n||_2 (true scale)
     double tol;
     int64_t itermax;
-    // diagnostics of the last iteration
-    cplx alpha, beta, w;
 };
 
 // Pointers/sizes passed by value to every kernel.
@@ -116,25 +113,28 @@ struct KParams {
     int32_t bicg, full;
     int32_t a_is_b;
     int32_t flags;
-    cplx *r[3];          // rotating seed residual buffers, r_n = r[n_started % 3] before start(n)
+    cplx *r[3];          // rotating seed residual buffers
     cplx *t[3];          // shadow (BiCG)
     cplx *q, *qt;        // H r, H t (raw, i.e. applied to stored vectors)
     const cplx *left;    // [nl][M] (== b when a = b)
     cplx *part_w;        // [nblk_spmv]
     cplx *part_u;        // [nblk_upd][2 + nl]
-    int32_t nblk_spmv, nblk_upd;
+    int32_t nblk_spmv, nblk_upd;   // worker CTAs (= partial count) of the SpMV / update kernels
     // per-shift arrays [nz]
     const cplx *z;
-    cplx *pi, *pi_old;
+    cplx *pibuf;         // [3][nz] rotating pi_n^k
+    cplx *pi_frozen;     // [nz] value at retirement
     uint8_t *active;
     double *res;
     int64_t *retired_at;
     cplx *u, *y;         // [nz][nl]
     cplx *g;             // [nl] projection of current r (true scale)
+    int32_t *act_list;   // [nz] compacted active shifts (ascending)
+    int32_t *n_act;      // [1]
     // full mode
     cplx *p, *x;         // [nz][M]
-    cplx *coef;          // [nz][3]: (sr/pi_n, beta^k_{n-1}, alpha^k_n) for active list order
-    int32_t *act_list;   // [nz]
-    int32_t *n_act_list; // [1]
-    int64_t *dbg_ts;     // optional [16] %globaltimer stamps of the scalar kernel phases
+    int64_t *dbg_ts;     // optional [16] %globaltimer stamps
+    uint32_t *ticket;    // [1] last-CTA detection in the SpMV kernel (reset by the last CTA)
 };
+
+enum { ST_ITERATING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };

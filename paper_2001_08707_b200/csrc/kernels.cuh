@@ -1,22 +1,21 @@
-// kernels.cuh — launch wrappers of the hot-path kernels (implemented in kernels.cu).
+// kernels.cuh — launch wrappers of the hot-path kernels (spmv.cu, update.cu, scalar.cu).
 #pragma once
 #include "common.cuh"
 
 namespace sk {
 
 constexpr int kThreads = 256;          // streaming kernels
-constexpr int kScalarThreads = 1024;   // the single-CTA scalar kernel
+constexpr int kScalarThreads = 1024;   // the single-CTA init / finish kernel
 constexpr int kMaxBlocks = 148 * 8;    // grid cap for grid-stride streaming kernels
+constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
 
-// Scalar-kernel phases.
-enum : int { PH_INIT = 1, PH_FINISH = 2, PH_START = 4 };
-
-constexpr int kTileBitsPublic = 10;  // Heisenberg tile: 2^10 states per CTA
 int stream_blocks(int64_t M);
-int heisenberg_blocks(int L, int64_t M);   // grid (and partial count) of the Heisenberg SpMV
+int heisenberg_blocks(int L, int64_t M);        // worker CTAs (= partials) of the Heisenberg SpMV
+int update_blocks(int64_t M, int nl, int full); // worker CTAs (= partials) of the update
 
 // SpMV q = H r (and qt = H t for BiCG) with the fused partial dot w = <tv, q>.
-// When `st` is null the kernel runs standalone on r0/t0 (sk_apply_operator) without partials.
+// Solver mode (st != null): CTA 0 runs the finish step, the last CTA the seed step.
+// Standalone mode (st == null, sk_apply_operator): r[0] -> q, no partials.
 struct SpmvArgs {
     const DevState *st;
     const cplx *r[3];
@@ -26,20 +25,22 @@ struct SpmvArgs {
     int64_t M;
     int bicg;
 };
-cudaError_t launch_heisenberg(const SpmvArgs &a, int L, double J, int nblk, cudaStream_t s);
-cudaError_t launch_csr(const SpmvArgs &a, const int64_t *row_ptr, const int32_t *col,
-                       const void *val, bool cplx_val, double avg_nnz, int nblk, cudaStream_t s);
-
-// Reverse-communication dot: part_w = <tv, q> on caller-supplied q (and qt ignored).
-cudaError_t launch_rc_dot(const KParams &kp, const cplx *q, cudaStream_t s);
+cudaError_t launch_heisenberg(const SpmvArgs &a, const KParams &kp, int L, double J, cudaStream_t s);
+cudaError_t launch_csr(const SpmvArgs &a, const KParams &kp, const int64_t *row_ptr, const int32_t *col,
+                       const void *val, bool cplx_val, double avg_nnz, cudaStream_t s);
+// Reverse communication: a.q holds the caller's q = H r.
+cudaError_t launch_rc_dot(const SpmvArgs &a, const KParams &kp, cudaStream_t s);
 
 // r_0 = b, t_0 = conj(b); partials of rho_0, nu_0, g_0 into part_u.
 cudaError_t launch_init(const KParams &kp, const cplx *b, cudaStream_t s);
 
-// Fused three-term update (+ shadow) + next-iteration dots + (full mode) all-shift x/p update.
+// Fused three-term update (+ shadow) + next-iteration dots + (full mode) all-shift x/p update;
+// CTA 0 runs the per-shift recurrences.
 cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s);
 
-// Single-CTA scalar step (reductions of partials, recurrences, retirement, seed switch).
-cudaError_t launch_scalar(const KParams &kp, int phases, cudaStream_t s);
+// Single-CTA steps outside the iteration: INIT (after launch_init) and FINISH (residuals,
+// retirement, switch of a pending iteration).
+enum : int { PH_INIT = 1, PH_FINISH = 2 };
+cudaError_t launch_scalar(const KParams &kp, int phase, cudaStream_t s);
 
 }  // namespace sk

@@ -1,0 +1,214 @@
+// update.cu — a5 + a7 of one iteration: the fused three-term seed update
+//   r_{n+1} = (1 + c - alpha z_s) r_n + alpha q - c r_{n-1}      (EQ-CG-RN-3REC P:L269, A r = z_s r - q)
+//   (BiCG shadow with conjugated coefficients)
+// with the reductions of the next iteration (rho_{n+1}, ||r_{n+1}||^2, a_l^dagger r_{n+1}) and,
+// in full mode, the all-shift update p^k = r_n/pi^k + beta^k p^k, x^k += alpha^k p^k
+// (EQ-SHIFTEDCG-x/p P:L327-328) for every active shift in the same pass over r_n.
+// CTA 0 is the shift agent: the projected per-shift recurrences (steps.cuh shift_step) run
+// beside the streaming CTAs.
+#include "kernels.cuh"
+#include "steps.cuh"
+
+namespace sk {
+
+int update_blocks(int64_t M, int nl, int full) {
+    const int R = full ? 1 : (nl <= 4 ? 2 : 1);
+    int64_t b = (M + (int64_t)kThreads * R - 1) / ((int64_t)kThreads * R);
+    const int64_t cap = 148 * 4;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+template <int NLMAX>
+__global__ void __launch_bounds__(kThreads) init_kernel(KParams kp, const cplx *__restrict__ b) {
+    cplx acc[2 + NLMAX];
+#pragma unroll
+    for (int j = 0; j < 2 + NLMAX; ++j) acc[j] = mk(0.0, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < kp.M;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const cplx bi = b[i];
+        kp.r[0][i] = bi;
+        if (kp.bicg) kp.t[0][i] = cconj(bi);   // r~_0 = conj(b)  (R3)
+        acc[0] = cfma(bi, bi, acc[0]);          // rho_0 = <r~_0, r_0> = sum b_i^2 for both methods
+        acc[1].x = fma(bi.x, bi.x, fma(bi.y, bi.y, acc[1].x));
+#pragma unroll
+        for (int l = 0; l < NLMAX; ++l)
+            if (l < kp.nl) acc[2 + l] = cfma_conj(kp.left[(int64_t)l * kp.M + i], bi, acc[2 + l]);
+    }
+    __shared__ cplx scratch[(2 + NLMAX) * (kThreads / 32)];
+    block_sum<2 + NLMAX>(acc, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < 2 + NLMAX; ++j)
+            if (j < 2 + kp.nl) kp.part_u[(int64_t)blockIdx.x * (2 + kp.nl) + j] = acc[j];
+    }
+}
+
+// ============================================================================ fused update
+// Each thread owns R rows per sweep (rows tid, tid+256, ... of a 256*R chunk) and issues all of
+// their loads before any arithmetic, so 4R+ independent 16-byte loads are in flight per thread.
+template <int NLMAX, bool BICG, bool FULL, int R>
+__global__ void __launch_bounds__(kThreads, FULL ? 2 : 4)
+update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
+    extern __shared__ cplx dyn[];  // FULL: coef[3 * n_act], then act list (int32)
+    DevState *st = kp.st;
+    if (st->status != ST_ITERATING) return;
+    if (blockIdx.x == 0) {          // shift agent (a4 + a6), beside the streaming CTAs
+        shift_step(kp);
+        return;
+    }
+    const int wb = blockIdx.x - 1, nwb = gridDim.x - 1;
+    const int64_t ns = st->n_started;            // seed step of iteration n ran: ns = n + 1
+    const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);
+    const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);
+    cplx *__restrict__ rn_ = pick3(kp.r, ns);
+    const cplx *__restrict__ tc_ = pick3(kp.t, ns + 2);
+    const cplx *__restrict__ tp_ = pick3(kp.t, ns + 1);
+    cplx *__restrict__ tn_ = pick3(kp.t, ns);
+    const cplx a_cur = st->a_cur, a_q = st->a_q, a_prev = st->a_prev;
+    const cplx ac_cur = cconj(a_cur), ac_q = cconj(a_q), ac_prev = cconj(a_prev);
+    int nact = 0;
+    cplx *coef = dyn;
+    int *act = nullptr;
+    if (FULL) {
+        // every streaming CTA evaluates the coefficients of the active shifts itself (the same
+        // arithmetic as the shift agent, so bit-identical): p^k = sr_n r_stored / pi_n^k + ...
+        nact = *kp.n_act;
+        act = (int *)(dyn + 3 * kp.nz);
+        const int64_t n = st->n;
+        const cplx *cur = kp.pibuf + (size_t)(n % 3) * kp.nz;
+        const cplx *prv = kp.pibuf + (size_t)((n + 2) % 3) * kp.nz;
+        const cplx alpha = st->alpha, beta = st->beta, c = st->c, zs = st->zs, sr = st->sr_it;
+        for (int j = threadIdx.x; j < nact; j += blockDim.x) {
+            const int k = kp.act_list[j];
+            const ShiftCoef sc = shift_coef(cur[k], prv[k], kp.z[k], zs, alpha, beta, c, n);
+            act[j] = k;
+            coef[3 * j] = cmul(sr, sc.ipik);
+            coef[3 * j + 1] = sc.bk;
+            coef[3 * j + 2] = sc.ak;
+        }
+        __syncthreads();
+    }
+    cplx acc[2 + NLMAX];
+#pragma unroll
+    for (int j = 0; j < 2 + NLMAX; ++j) acc[j] = mk(0.0, 0.0);
+    const int64_t M = kp.M;
+    const int nl = kp.nl;
+    const int64_t chunk = (int64_t)kThreads * R;
+    for (int64_t base = (int64_t)wb * chunk; base < M; base += (int64_t)nwb * chunk) {
+        cplx rc[R], rp[R], qi[R], tc[R], tp[R], qti[R], lv[R][NLMAX];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
+            if (i < M) {
+                rc[k] = ldg_cs(rc_ + i);
+                rp[k] = ldg_cs(rp_ + i);
+                qi[k] = ldg_cs(q + i);
+                if (BICG) { tc[k] = ldg_cs(tc_ + i); tp[k] = ldg_cs(tp_ + i); qti[k] = ldg_cs(qt + i); }
+#pragma unroll
+                for (int l = 0; l < NLMAX; ++l)
+                    if (l < nl) lv[k][l] = ldg_cs(kp.left + (int64_t)l * M + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
+            if (i >= M) continue;
+            cplx rn = cmul(a_cur, rc[k]);
+            rn = cfma(a_q, qi[k], rn);
+            rn = cfma(a_prev, rp[k], rn);
+            rn_[i] = rn;
+            if (BICG) {
+                cplx tn = cmul(ac_cur, tc[k]);
+                tn = cfma(ac_q, qti[k], tn);
+                tn = cfma(ac_prev, tp[k], tn);
+                tn_[i] = tn;
+                acc[0] = cfma_conj(tn, rn, acc[0]);
+            } else {
+                acc[0] = cfma(rn, rn, acc[0]);
+            }
+            acc[1].x = fma(rn.x, rn.x, fma(rn.y, rn.y, acc[1].x));
+#pragma unroll
+            for (int l = 0; l < NLMAX; ++l)
+                if (l < nl) acc[2 + l] = cfma_conj(lv[k][l], rn, acc[2 + l]);
+            if (FULL) {
+                const cplx r0 = rc[k];
+                int j = 0;
+                for (; j + 4 <= nact; j += 4) {
+                    cplx pk[4], xk[4];
+#pragma unroll
+                    for (int uu = 0; uu < 4; ++uu) {
+                        const int64_t off = (int64_t)act[j + uu] * M + i;
+                        pk[uu] = ldg_cs(kp.p + off);
+                        xk[uu] = ldg_cs(kp.x + off);
+                    }
+#pragma unroll
+                    for (int uu = 0; uu < 4; ++uu) {
+                        const int64_t off = (int64_t)act[j + uu] * M + i;
+                        cplx pn = cmul(coef[3 * (j + uu)], r0);
+                        pn = cfma(coef[3 * (j + uu) + 1], pk[uu], pn);
+                        stg_cs(kp.p + off, pn);
+                        stg_cs(kp.x + off, cfma(coef[3 * (j + uu) + 2], pn, xk[uu]));
+                    }
+                }
+                for (; j < nact; ++j) {
+                    const int64_t off = (int64_t)act[j] * M + i;
+                    const cplx pk = ldg_cs(kp.p + off), xk = ldg_cs(kp.x + off);
+                    cplx pn = cmul(coef[3 * j], r0);
+                    pn = cfma(coef[3 * j + 1], pk, pn);
+                    stg_cs(kp.p + off, pn);
+                    stg_cs(kp.x + off, cfma(coef[3 * j + 2], pn, xk));
+                }
+            }
+        }
+    }
+    __shared__ cplx scratch[(2 + NLMAX) * (kThreads / 32)];
+    block_sum<2 + NLMAX>(acc, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < 2 + NLMAX; ++j)
+            if (j < 2 + kp.nl) kp.part_u[(int64_t)wb * (2 + kp.nl) + j] = acc[j];
+    }
+}
+
+template <int NLMAX, bool BICG, bool FULL>
+static cudaError_t launch_update_t(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
+    constexpr int R = FULL ? 1 : (NLMAX <= 4 ? 2 : 1);   // must match update_blocks()
+    const size_t shm = FULL ? (size_t)kp.nz * (3 * sizeof(cplx) + sizeof(int)) : 0;
+    if (FULL && shm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(update_kernel<NLMAX, BICG, FULL, R>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (e != cudaSuccess) return e;
+    }
+    update_kernel<NLMAX, BICG, FULL, R><<<kp.nblk_upd + 1, kThreads, shm, s>>>(kp, q, qt);
+    return cudaGetLastError();
+}
+
+template <int NLMAX>
+static cudaError_t launch_update_nl(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
+    if (kp.full)
+        return kp.bicg ? launch_update_t<NLMAX, true, true>(kp, q, qt, s)
+                       : launch_update_t<NLMAX, false, true>(kp, q, qt, s);
+    return kp.bicg ? launch_update_t<NLMAX, true, false>(kp, q, qt, s)
+                   : launch_update_t<NLMAX, false, false>(kp, q, qt, s);
+}
+
+cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
+    if (kp.nl <= 1) return launch_update_nl<1>(kp, q, qt, s);
+    if (kp.nl <= 4) return launch_update_nl<4>(kp, q, qt, s);
+    if (kp.nl <= 8) return launch_update_nl<8>(kp, q, qt, s);
+    if (kp.nl <= 16) return launch_update_nl<16>(kp, q, qt, s);
+    return launch_update_nl<32>(kp, q, qt, s);
+}
+
+cudaError_t launch_init(const KParams &kp, const cplx *b, cudaStream_t s) {
+    if (kp.nl <= 1) init_kernel<1><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
+    else if (kp.nl <= 4) init_kernel<4><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
+    else if (kp.nl <= 8) init_kernel<8><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
+    else if (kp.nl <= 16) init_kernel<16><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
+    else init_kernel<32><<<kp.nblk_upd, kThreads, 0, s>>>(kp, b);
+    return cudaGetLastError();
+}
+
+}  // namespace sk
