@@ -222,7 +222,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
     kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M) : sk::stream_blocks(M);
-    kp.nblk_upd = sk::update_blocks(M, c->nl, c->full);
+    kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
+    kp.n_agents = sk::shift_agents(c->nz);
     const size_t vb = (size_t)M * sizeof(cplx);
 
     // One device arena for everything the context owns (one cudaMalloc / cudaFree); every
@@ -247,14 +248,13 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&kp.pibuf, sizeof(cplx) * 3 * c->nz);
         add(&kp.pi_frozen, sizeof(cplx) * c->nz);
         add(&kp.ticket, sizeof(uint32_t));
+        add(&kp.amin_part, sizeof(AminPart) * 8);
         add(&kp.active, c->nz);
         add(&kp.res, sizeof(double) * c->nz);
         add(&kp.retired_at, sizeof(int64_t) * c->nz);
         add(&kp.u, sizeof(cplx) * c->nz * c->nl);
         add(&kp.y, sizeof(cplx) * c->nz * c->nl);
         add(&kp.g, sizeof(cplx) * c->nl);
-        add(&kp.act_list, sizeof(int32_t) * c->nz);
-        add(&kp.n_act, sizeof(int32_t));
         if (getenv("SHIFTK_DEBUG_TS")) add(&kp.dbg_ts, sizeof(int64_t) * 16);
         if (!c->a_is_b && p->left_mem != SK_MEM_DEVICE) add(&c->left_owned, vb * c->nl);
         if (c->full) {
@@ -490,7 +490,9 @@ int sk_get_shift_state(sk_ctx *c, sk_cplx *pi, uint8_t *active, int64_t *retired
     CK(cudaMemcpyAsync(ret.data(), c->kp.retired_at, sizeof(int64_t) * c->nz, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     for (int k = 0; k < c->nz; ++k) {
-        const cplx v = act[k] ? cur[k] : frozen[k];   // retired shifts report pi at retirement
+        const cplx bs = c->st_host->bscale[n % 3];   // lazy buffer scale (seed switches)
+        const cplx v = act[k] ? mk(cur[k].x * bs.x - cur[k].y * bs.y, cur[k].x * bs.y + cur[k].y * bs.x)
+                              : frozen[k];   // retired shifts report pi at retirement
         if (pi) pi[k] = {v.x, v.y};
         if (active) active[k] = act[k];
         if (retired_at) retired_at[k] = ret[k];

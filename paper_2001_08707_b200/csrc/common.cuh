@@ -80,7 +80,10 @@ __host__ __device__ __forceinline__ T pick3(T const (&a)[3], int64_t i) {
 // read from here, so a captured CUDA graph can replay iterations without host involvement.
 //
 // Iteration bookkeeping: `n` completed iterations.  r_n lives in r[n % 3] (stored form,
-// r_true = sr_cur * r_stored); pi_n^k in pibuf[n % 3][k], pi_{n-1} in pibuf[(n + 2) % 3].
+// r_true = sr_cur * r_stored).  pi_n^k = pibuf[n % 3][k] * bscale[n % 3] and
+// pi_{n-1}^k = pibuf[(n + 2) % 3][k] * bscale[(n + 2) % 3]: a seed switch rescales the two
+// buffers' scale factors, never their elements (O(1) instead of O(N_z)).
+// Retirement after a finish is applied lazily by the next per-shift pass (lz_pending).
 // ---------------------------------------------------------------------------------------------
 struct DevState {
     int64_t n;           // completed iterations
@@ -100,6 +103,11 @@ struct DevState {
     cplx alpha, beta, c; // seed scalars of the current iteration (read by the shift step)
     cplx sr_it;          // sr_cur used by the current iteration (full-mode coefficient)
     cplx w;              // diagnostics
+    cplx bscale[3];      // lazy scale factors of the three pi buffers
+    int32_t lz_pending;  // a retirement test of iteration lz_iter is due
+    int32_t pad_;
+    double lz_nu;        // ||r|| (current normalisation) for the pending retirement test
+    int64_t lz_iter;
     double nu;           // ||r_n||_2 (true scale)
     double tol;
     int64_t itermax;
@@ -129,12 +137,19 @@ struct KParams {
     int64_t *retired_at;
     cplx *u, *y;         // [nz][nl]
     cplx *g;             // [nl] projection of current r (true scale)
-    int32_t *act_list;   // [nz] compacted active shifts (ascending)
-    int32_t *n_act;      // [1]
     // full mode
     cplx *p, *x;         // [nz][M]
     int64_t *dbg_ts;     // optional [16] %globaltimer stamps
     uint32_t *ticket;    // [1] last-CTA detection in the SpMV kernel (reset by the last CTA)
+    int32_t n_agents;    // shift-agent CTAs of the update kernel (each a slice of the shifts)
+    struct AminPart *amin_part;   // [n_agents] per-agent argmin |pi_{n+1}| and survivor count
+};
+
+// Per shift-agent result: argmin over its slice of |pi_{n+1}|^2 (lowest index on ties).
+struct AminPart {
+    double a2;
+    int32_t idx, cnt;
+    cplx f, fp;          // pi_{n+1}, pi_n of that shift
 };
 
 enum { ST_ITERATING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };

@@ -11,7 +11,8 @@ constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
 
 int stream_blocks(int64_t M);
 int heisenberg_blocks(int L, int64_t M);        // worker CTAs (= partials) of the Heisenberg SpMV
-int update_blocks(int64_t M, int nl, int full); // worker CTAs (= partials) of the update
+int update_blocks(int64_t M, int nl, int full, int nz); // worker CTAs (= partials) of the update
+int shift_agents(int nz);                        // shift-agent CTAs of the update
 
 // SpMV q = H r (and qt = H t for BiCG) with the fused partial dot w = <tv, q>.
 // Solver mode (st != null): CTA 0 runs the finish step, the last CTA the seed step.

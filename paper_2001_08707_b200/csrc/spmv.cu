@@ -37,9 +37,12 @@ __device__ __forceinline__ bool spmv_enter(const SpmvArgs &a, bool &agent, int &
     if (!a.st) return true;
     if (a.st->status != ST_ITERATING) return false;
     buf = (int)(a.st->n_started % 3);
+    if (blockIdx.x == 1) dbg_stamp(kp.dbg_ts, 0);                 // first worker CTA starts
     if (blockIdx.x == 0) {
         agent = true;
-        if (a.st->pending) finish_step(kp, sc);
+        dbg_stamp(kp.dbg_ts, 1);
+        if (a.st->pending) finish_step(kp, sc, /*eager=*/false);
+        dbg_stamp(kp.dbg_ts, 2);                                   // finish agent done
     }
     return true;
 }
@@ -59,14 +62,19 @@ __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParams &kp, 
     if (threadIdx.x == 0) last = (atomicAdd(kp.ticket, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!last) return;
+    dbg_stamp(kp.dbg_ts, 3);                                       // last CTA arrives
     __threadfence();
-    state_load(sc.S, kp.st);
-    reduce_columns(a.part_w, gridDim.x - 1, 1, 0, 1, sc);
+    state_load_nosync(sc.S, kp.st);
+    reduce_columns(a.part_w, gridDim.x - 1, 1, 1, sc);   // (its barriers publish sc.S)
     if (threadIdx.x == 0) {
         if (sc.S.status == ST_ITERATING) seed_step(&sc.S, sc.col[0], a.bicg);
         *kp.ticket = 0u;
     }
+    __syncthreads();
+    // breakdown ends the run here: apply the pending retirement test so results are final
+    if (sc.S.status == ST_BREAKDOWN && sc.S.lz_pending) retire_pass(kp, sc);
     state_store(kp.st, sc.S);
+    dbg_stamp(kp.dbg_ts, 4);                                       // seed step done
 }
 
 // ============================================================================ Heisenberg H.v

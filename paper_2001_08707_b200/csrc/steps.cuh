@@ -16,6 +16,10 @@
 // Because seed switching is applied lazily (scale factors, no vector pass), the SpMV of
 // iteration n+1 does not depend on the finish of iteration n, which is what lets the finish
 // run beside it.
+//
+// Latency rule used throughout (measured: one dependent L2/DRAM round trip costs ~0.5-1 us):
+// every loop issues all of its loads for a block of shifts before any dependent arithmetic or
+// branch, so a step over N_z shifts costs ~N_z/(4*256) round trips, not N_z/256 * (chain).
 #pragma once
 #include "common.cuh"
 
@@ -44,41 +48,53 @@ static __device__ __noinline__ double xabs(cplx b) {
 constexpr int kStateWords = sizeof(DevState) / 8;
 static_assert(sizeof(DevState) % 8 == 0, "DevState is copied as 8-byte words");
 static_assert(kStateWords <= 256, "DevState copy uses one word per thread");
-static __device__ __forceinline__ void state_load(DevState &dst, const DevState *src) {
+static __device__ __forceinline__ void state_load_nosync(DevState &dst, const DevState *src) {
     if (threadIdx.x < kStateWords)
         ((long long *)&dst)[threadIdx.x] = __ldcg((const long long *)src + threadIdx.x);
-    __syncthreads();
 }
 static __device__ __forceinline__ void state_store(DevState *dst, const DevState &src) {
     __syncthreads();
     if (threadIdx.x < kStateWords) ((long long *)dst)[threadIdx.x] = ((const long long *)&src)[threadIdx.x];
 }
 
+constexpr int kSpt = 4;             // shifts per thread per block of a step loop
+constexpr int kSmemShifts = 4096;   // shifts whose active flags fit in the scratch copy
+
 // Shared scratch of the step functions (one instance per CTA that runs them).
 struct StepScratch {
-    DevState S;        // shared copy of the device state
-    cplx col[40];      // reduced partial columns
-    cplx red[4][32];   // per-warp partial sums (4 columns at a time)
+    DevState S;                  // shared copy of the device state
+    cplx col[40];                // reduced partial columns
+    cplx red[4][32];             // per-warp partial sums (4 columns at a time)
     double rd[32];
     int ri[32], rc[32];
     cplx bc[4];
     int bi[4];
+    uint8_t act[kSmemShifts];    // active flags after retirement (compaction source)
 };
 
-// Sum columns [c0, c0 + ncol) of part[nblk][stride] into sc.col[c0 ..] — fixed order
-// (per-thread strided sum, then warps in index order): deterministic.  Up to four columns per
-// sweep so that their loads are in flight together.  All threads of the CTA must call it.
-static __device__ __forceinline__ void reduce_columns(const cplx *part, int nblk, int stride, int c0,
-                                               int ncol, StepScratch &sc) {
+// Sum columns [0, ncol) of part[nblk][stride] into sc.col — fixed order (per-thread strided
+// sum over b = tid + 4k*NT.., then warps in index order): deterministic.  Loads of 4 blocks x
+// up to 4 columns are issued before they are summed.  All threads call it; ends with a barrier.
+static __device__ __forceinline__ void reduce_columns(const cplx *part, int nblk, int stride, int ncol,
+                                                      StepScratch &sc) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int NT = blockDim.x;
     for (int cb = 0; cb < ncol; cb += 4) {
         const int nc = ncol - cb < 4 ? ncol - cb : 4;
         cplx v[4] = {mk(0, 0), mk(0, 0), mk(0, 0), mk(0, 0)};
-        for (int b = tid; b < nblk; b += blockDim.x) {
-            const cplx *row = part + (int64_t)b * stride + c0 + cb;
+        for (int b0 = tid; b0 < nblk; b0 += 4 * NT) {
+            cplx x[4][4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (j < nc) v[j] = cadd(v[j], ldcg(row + j));
+            for (int m = 0; m < 4; ++m) {
+                const int b = b0 + m * NT;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    x[m][j] = (b < nblk && j < nc) ? ldcg(part + (int64_t)b * stride + cb + j) : mk(0, 0);
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = cadd(v[j], x[m][j]);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -89,20 +105,22 @@ static __device__ __forceinline__ void reduce_columns(const cplx *part, int nblk
         if (tid < nc) {
             cplx s = sc.red[tid][0];
             for (int w = 1; w < nw; ++w) s = cadd(s, sc.red[tid][w]);
-            sc.col[c0 + cb + tid] = s;
+            sc.col[cb + tid] = s;
         }
         __syncthreads();
     }
 }
 
 // Block exclusive scan of 0/1 flags over [0, n) in chunks of blockDim: writes the compacted
-// ascending index list, returns the count (all threads).
-static __device__ __forceinline__ int compact_active(const uint8_t *act, int n, int32_t *list, StepScratch &sc) {
+// ascending index list, returns the count (all threads).  Flags come from shared memory when
+// n <= kSmemShifts (the caller filled sc.act), else from `act_g`.
+static __device__ int compact_active(const uint8_t *act_g, int n, int32_t *list, StepScratch &sc) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const bool sm = n <= kSmemShifts;
     int total = 0;
     for (int base = 0; base < n; base += blockDim.x) {
         const int k = base + tid;
-        const int a = (k < n) ? (int)act[k] : 0;
+        const int a = (k < n) ? (int)(sm ? sc.act[k] : act_g[k]) : 0;
         const unsigned bal = __ballot_sync(0xffffffffu, a);
         if (lane == 0) sc.ri[warp] = __popc(bal);
         __syncthreads();
@@ -125,103 +143,134 @@ static __device__ __forceinline__ int compact_active(const uint8_t *act, int n, 
     return total;
 }
 
-// ------------------------------------------------------------------------------- finish_step
-// Finishes iteration m = S->n (pending): consumes the update partials of r_{m+1}.  All threads
-// of the CTA call it; reads and writes the device state in global memory.
-static __device__ void finish_step(const KParams &kp, StepScratch &sc) {
-    state_load(sc.S, kp.st);
+// ------------------------------------------------------------------------------- retirement
+// The retirement test of iteration it = S->lz_iter: res_k = ||r_it|| / |pi_it^k|
+// (EQ-COLLINEAR P:L300), retire when res_k < tol (R8).  Evaluated with the pi buffer
+// of iteration it and its lazy scale, so every evaluator (shift agent, full-mode streaming
+// CTAs, eager pass) takes the identical decision.
+static __device__ __forceinline__ bool retire_test(double lz_nu, cplx pik, double tol, double &res) {
+    res = lz_nu / sqrt(cabs2(pik));
+    return res < tol;
+}
+
+// Eager application of a pending retirement test to every active shift (CTA-wide; operates on
+// the shared state copy sc.S; the caller stores it).  Used when no further per-shift pass will
+// run: the stand-alone finish, terminal states, breakdown.
+static __device__ void retire_pass(const KParams &kp, StepScratch &sc) {
     DevState *S = &sc.S;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int nz = kp.nz, nl = kp.nl, nred = 2 + nl;
-    reduce_columns(kp.part_u, kp.nblk_upd, nred, 0, nred, sc);
+    const int NT = blockDim.x, nz = kp.nz;
+    int cnt = 0;
+    if (S->lz_pending && S->lz_iter == S->n) {
+        const int64_t it = S->lz_iter;
+        const cplx *buf = kp.pibuf + (size_t)(it % 3) * nz;
+        const cplx bs = S->bscale[it % 3];
+        const double lz_nu = S->lz_nu, tol = S->tol;
+        for (int k0 = tid; k0 < nz; k0 += kSpt * NT) {
+            uint8_t a[kSpt];
+            cplx pk[kSpt];
+#pragma unroll
+            for (int s = 0; s < kSpt; ++s) {          // all loads of the block first
+                const int k = k0 + s * NT;
+                a[s] = k < nz ? kp.active[k] : (uint8_t)0;
+                pk[s] = k < nz ? buf[k] : mk(1, 0);
+            }
+#pragma unroll
+            for (int s = 0; s < kSpt; ++s) {
+                const int k = k0 + s * NT;
+                if (k >= nz || !a[s]) continue;
+                const cplx p = cmul(pk[s], bs);
+                double rk;
+                if (retire_test(lz_nu, p, tol, rk)) {
+                    kp.active[k] = 0;
+                    kp.retired_at[k] = it;
+                    kp.pi_frozen[k] = p;
+                } else {
+                    ++cnt;
+                }
+                kp.res[k] = rk;
+            }
+        }
+    } else {
+        for (int k = tid; k < nz; k += NT) cnt += kp.active[k] ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) sc.rc[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        int c = 0;
+        for (int w = 0; w < nw; ++w) c += sc.rc[w];
+        S->n_active = c;
+        S->lz_pending = 0;
+        if (c == 0) S->status = ST_CONVERGED;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------------- finish_step
+// Finishes iteration m = S->n (pending): consumes the update partials of r_{m+1} and the
+// argmin of |pi_{m+1}| found by the shift step of iteration m.  O(1) work besides the partial
+// reduction: the switch rescales buffer scale factors, and the retirement test is left pending
+// for the next per-shift pass (eager = true applies it here).  Retirement removes the shifts
+// with the LARGEST |pi| (res = nu/|pi| < tol), so the argmin over the survivors is the argmin
+// over the shifts active before the test unless every shift retires — which is exactly the
+// test nu/|pi_{s*}| < tol on that argmin (R10, R11).
+static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eager) {
+    state_load_nosync(sc.S, kp.st);
+    DevState *S = &sc.S;
+    const int nl = kp.nl, nred = 2 + nl;
+    reduce_columns(kp.part_u, kp.nblk_upd, nred, nred, sc);   // (its barriers publish sc.S)
     const int64_t m = S->n;
-    cplx *cur = kp.pibuf + (size_t)((m + 1) % 3) * nz;   // pi_{m+1}
-    cplx *prv = kp.pibuf + (size_t)(m % 3) * nz;         // pi_m
-    const double nu2 = sc.col[1].x;
-    const double nu = sqrt(nu2);
-    const double tol = S->tol;
-    // a8: residuals and retirement; local count + argmin of |pi|^2 over survivors
-    int cnt = 0, bi = -1;
-    double best = 0.0;
-    for (int k = tid; k < nz; k += blockDim.x) {
-        if (!kp.active[k]) continue;
-        const cplx pk = cur[k];
-        const double a2 = cabs2(pk);
-        const double rk = nu * rsqrt(a2);      // ||r_{m+1}|| / |pi_{m+1}^k|
-        kp.res[k] = rk;
-        if (rk < tol) {
-            kp.active[k] = 0;
-            kp.retired_at[k] = m + 1;
-            kp.pi_frozen[k] = pk;
-            continue;
+    const double nu = sqrt(sc.col[1].x);
+    if (threadIdx.x == 0) {
+        // argmin over the shift agents' slices (ascending: ties keep the lowest index)
+        AminPart best = kp.amin_part[0];
+        int survivors = best.cnt;
+        for (int a = 1; a < kp.n_agents; ++a) {
+            const AminPart p = kp.amin_part[a];
+            survivors += p.cnt;
+            if (p.idx >= 0 && (best.idx < 0 || p.a2 < best.a2)) best = p;
         }
-        ++cnt;
-        if (bi < 0 || a2 < best) { best = a2; bi = k; }   // ascending k: ties keep the lowest
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (oi >= 0 && (bi < 0 || ov < best || (ov == best && oi < bi))) { best = ov; bi = oi; }
-    }
-    if (lane == 0) { sc.rc[warp] = cnt; sc.rd[warp] = best; sc.ri[warp] = bi; }
-    __syncthreads();
-    if (warp == 0) {
-        int c = lane < nw ? sc.rc[lane] : 0;
-        double b = lane < nw ? sc.rd[lane] : 0.0;
-        int i = lane < nw ? sc.ri[lane] : -1;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            c += __shfl_xor_sync(0xffffffffu, c, o);
-            const double ov = __shfl_xor_sync(0xffffffffu, b, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-            if (oi >= 0 && (i < 0 || ov < b || (ov == b && oi < i))) { b = ov; i = oi; }
-        }
-        if (lane == 0) { sc.bi[0] = c; sc.bi[1] = i; }
-    }
-    __syncthreads();
-    cnt = sc.bi[0];
-    const int bst = sc.bi[1];
-    const bool sw = cnt > 0 && !(kp.flags & 1) && bst != S->seed;
-    cplx rf = mk(1, 0), rfp = mk(1, 0);
-    if (sw) {   // a9 / R9: the new seed's r, r_prev, pi, alpha, rho in its own normalisation
-        const cplx f = cur[bst], fp = prv[bst];
-        rf = xrecip(f);
-        rfp = xrecip(fp);
-        __syncthreads();   // everyone has read pi[best] before it is rescaled
-        for (int k = tid; k < nz; k += blockDim.x) {
-            if (!kp.active[k]) continue;   // retired shifts are not rescaled (R13)
-            cur[k] = cmul(cur[k], rf);
-            prv[k] = cmul(prv[k], rfp);
-        }
-        if (tid == 0) {
-            S->sr_cur = cmul(S->sr_cur, rf);                        // r_{m+1} /= f
-            S->sr_prev = cmul(S->sr_prev, rfp);                     // r_m /= f'
-            S->alpha_prev = cmul(S->alpha_prev, cmul(fp, rf));      // alpha_m^{s*}
-            S->rho_prev = cmul(S->rho_prev, cmul(rfp, rfp));        // rho_m / f'^2
+        S->n_active = survivors;
+        const cplx f = best.f, fp = best.fp;
+        const int bst = best.idx;
+        double rmin;
+        const bool all_retire = retire_test(nu, f, S->tol, rmin);
+        const bool sw = !all_retire && !(kp.flags & 1) && bst != S->seed;
+        cplx rf = mk(1, 0);
+        if (sw) {   // a9 / R9: the new seed's r, r_prev, pi, alpha, rho in its own normalisation
+            rf = xrecip(f);
+            const cplx rfp = xrecip(fp);
+            S->bscale[(m + 1) % 3] = cmul(S->bscale[(m + 1) % 3], rf);   // pi_{m+1} /= f
+            S->bscale[m % 3] = cmul(S->bscale[m % 3], rfp);               // pi_m /= f'
+            S->sr_cur = cmul(S->sr_cur, rf);                               // r_{m+1} /= f
+            S->sr_prev = cmul(S->sr_prev, rfp);                            // r_m /= f'
+            S->alpha_prev = cmul(S->alpha_prev, cmul(fp, rf));             // alpha_m^{s*}
+            S->rho_prev = cmul(S->rho_prev, cmul(rfp, rfp));               // rho_m / f'^2
             S->zs = kp.z[bst];
             S->seed = bst;
             S->nswitch += 1;
         }
-    }
-    if (tid < nl) kp.g[tid] = sw ? cmul(sc.col[2 + tid], rf) : sc.col[2 + tid];
-    const int nact = compact_active(kp.active, nz, kp.act_list, sc);
-    if (tid == 0) {
-        *kp.n_act = nact;
-        S->rho_cur = sw ? cmul(sc.col[0], cmul(rf, rf)) : sc.col[0];   // rho_{m+1} / f^2
-        S->nu = sw ? nu * sqrt(cabs2(rf)) : nu;
+        S->rho_cur = cmul(sc.col[0], cmul(rf, rf));                       // rho_{m+1} / f^2
+        S->nu = nu * sqrt(cabs2(rf));
+        S->lz_pending = 1;
+        S->lz_nu = S->nu;   // current normalisation (matches the rescaled pi buffers)
+        S->lz_iter = m + 1;
         S->n = m + 1;
         S->pending = 0;
-        S->n_active = cnt;
-        if (cnt == 0) S->status = ST_CONVERGED;
-        else if (m + 1 >= S->itermax) S->status = ST_MAXITER;
+        if (!all_retire && m + 1 >= S->itermax) S->status = ST_MAXITER;
+        sc.bc[0] = rf;
+        sc.bi[0] = all_retire || S->status != ST_ITERATING;
     }
+    __syncthreads();
+    if (threadIdx.x < nl) kp.g[threadIdx.x] = cmul(sc.col[2 + threadIdx.x], sc.bc[0]);
+    if (eager || sc.bi[0]) retire_pass(kp, sc);
     state_store(kp.st, sc.S);
 }
 
 // ------------------------------------------------------------------------------- seed_step
-// One thread, on a shared copy of the state.  w_raw = <r~|r, q> of the stored vectors.  Writes the update coefficients.
+// One thread, on a shared copy of the state.  w_raw = <r~|r, q> of the stored vectors.
 static __device__ void seed_step(DevState *S, cplx wraw, int bicg) {
     const cplx sr = S->sr_cur;
     const cplx w = cmul(cmul(sr, sr), wraw);   // true-scale w_n (shadow scale = conj(sr))
@@ -255,6 +304,7 @@ static __device__ void seed_step(DevState *S, cplx wraw, int bicg) {
     S->rho_prev = rho;
     S->n_started = n + 1;
     S->pending = 1;
+    S->bscale[(n + 1) % 3] = mk(1.0, 0.0);   // the shift step writes pi_{n+1} unscaled
     S->nspmv += bicg ? 2 : 1;
 }
 
@@ -264,7 +314,7 @@ struct ShiftCoef {
     cplx pin, ak, bk, ipik;
 };
 static __device__ __forceinline__ ShiftCoef shift_coef(cplx pik, cplx piok, cplx zk, cplx zs, cplx alpha,
-                                                cplx beta, cplx c, int64_t n) {
+                                                       cplx beta, cplx c, int64_t n) {
     ShiftCoef o;
     const cplx sigma = csub(zk, zs);
     // EQ-SHIFTEDCG-PI: pi_{n+1} = (1 + c + alpha sigma) pi_n - c pi_{n-1}
@@ -279,26 +329,140 @@ static __device__ __forceinline__ ShiftCoef shift_coef(cplx pik, cplx piok, cplx
     return o;
 }
 
-// Projected update of every active shift (a4 + a6); writes pi_{n+1}.  All threads call it.
-static __device__ void shift_step(const KParams &kp) {
-    const DevState *S = kp.st;
+// Per-shift pass of iteration n (a4 + a6, and the pending retirement test of a8): for every
+// shift active at the previous finish, apply the retirement test; for the survivors compute
+// pi_{n+1}, u, y; find argmin |pi_{n+1}| (lowest index on ties) for the next finish.  Shifts
+// are visited directly in blocks of 2 per thread with all loads issued first.  For
+// N_left > 1 the (shift, l) pairs of a block are spread over the threads.  All threads call
+// it.  Writes only per-shift arrays and the amin / n_active / lz_pending words of the state.
+struct ShiftScratch {
+    cplx g[32];
+    cplx ak[512], bk[512], ip[512];   // per-shift coefficients of a block (2 per thread, <= 256 threads)
+    uint8_t act[512];
+    double rd[32];
+    int ri[32], rc[32];
+    cplx f, fp;
+};
+static __device__ void shift_step(const KParams &kp, ShiftScratch &ss, int agent) {
+    DevState *S = kp.st;
     const int64_t n = S->n;
-    const int nz = kp.nz, nl = kp.nl;
-    const cplx *cur = kp.pibuf + (size_t)(n % 3) * nz;
-    const cplx *prv = kp.pibuf + (size_t)((n + 2) % 3) * nz;
-    cplx *nxt = kp.pibuf + (size_t)((n + 1) % 3) * nz;
+    const int nzt = kp.nz, nl = kp.nl, NT = blockDim.x, tid = threadIdx.x;
+    const int per = (nzt + kp.n_agents - 1) / kp.n_agents;   // this agent's slice [k_lo, k_lo+nz)
+    const int k_lo = agent * per;
+    const int nz = nzt - k_lo < per ? (nzt - k_lo > 0 ? nzt - k_lo : 0) : per;
+    const int lane = tid & 31, warp = tid >> 5, nw = NT >> 5;
+    const cplx *cur = kp.pibuf + (size_t)(n % 3) * nzt + k_lo;
+    const cplx *prv = kp.pibuf + (size_t)((n + 2) % 3) * nzt + k_lo;
+    cplx *nxt = kp.pibuf + (size_t)((n + 1) % 3) * nzt + k_lo;
+    const cplx *zz = kp.z + k_lo;
+    uint8_t *actv = kp.active + k_lo;
+    const cplx bc = S->bscale[n % 3], bp = S->bscale[(n + 2) % 3];
     const cplx alpha = S->alpha, beta = S->beta, c = S->c, zs = S->zs;
-    const int nact = *kp.n_act;
-    for (int j = threadIdx.x; j < nact; j += blockDim.x) {
-        const int k = kp.act_list[j];
-        const ShiftCoef sc = shift_coef(cur[k], prv[k], kp.z[k], zs, alpha, beta, c, n);
-        for (int l = 0; l < nl; ++l) {                                // P:L372-376 (R1)
-            const int64_t o = (int64_t)k * nl + l;
-            const cplx uu = cadd(cmul(kp.g[l], sc.ipik), cmul(sc.bk, kp.u[o]));
-            kp.u[o] = uu;
-            kp.y[o] = cfma(sc.ak, uu, kp.y[o]);
+    const bool lz = S->lz_pending != 0 && S->lz_iter == n;
+    const double lz_nu = S->lz_nu, tol = S->tol;
+    int cnt = 0, bi = -1;
+    double best = 0.0;
+    if (tid < nl) ss.g[tid] = kp.g[tid];
+    __syncthreads();
+    for (int k0 = 0; k0 < nz; k0 += 2 * NT) {
+        uint8_t a[2];
+        cplx pc[2], pp[2], zk[2], uk[2], yk[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {            // all loads of the block first
+            const int k = k0 + tid + s * NT;
+            const bool in = k < nz;
+            a[s] = in ? actv[k] : (uint8_t)0;
+            pc[s] = in ? cur[k] : mk(1, 0);
+            pp[s] = in ? prv[k] : mk(1, 0);
+            zk[s] = in ? zz[k] : mk(0, 0);
+            uk[s] = (in && nl == 1) ? kp.u[k_lo + k] : mk(0, 0);
+            yk[s] = (in && nl == 1) ? kp.y[k_lo + k] : mk(0, 0);
         }
-        nxt[k] = sc.pin;
+        if (nl > 1) __syncthreads();   // previous block's coefficients are consumed
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int k = k0 + tid + s * NT;
+            bool on = k < nz && a[s];
+            const cplx pik = cmul(pc[s], bc), piok = cmul(pp[s], bp);
+            if (on && lz) {
+                double rk;
+                if (retire_test(lz_nu, pik, tol, rk)) {
+                    on = false;
+                    actv[k] = 0;
+                    kp.retired_at[k_lo + k] = n;
+                    kp.pi_frozen[k_lo + k] = pik;
+                }
+                kp.res[k_lo + k] = rk;
+            }
+            if (nl > 1) ss.act[tid + s * NT] = on;
+            if (!on) continue;
+            const ShiftCoef sc = shift_coef(pik, piok, zk[s], zs, alpha, beta, c, n);
+            nxt[k] = sc.pin;
+            ++cnt;
+            const double a2 = cabs2(sc.pin);
+            if (bi < 0 || a2 < best) { best = a2; bi = k; }   // ascending k: ties keep the lowest
+            if (nl == 1) {
+                const cplx uu = cadd(cmul(ss.g[0], sc.ipik), cmul(sc.bk, uk[s]));   // P:L372-376 (R1)
+                kp.u[k_lo + k] = uu;
+                kp.y[k_lo + k] = cfma(sc.ak, uu, yk[s]);
+            } else {
+                ss.ak[tid + s * NT] = sc.ak;
+                ss.bk[tid + s * NT] = sc.bk;
+                ss.ip[tid + s * NT] = sc.ipik;
+            }
+        }
+        if (nl > 1) {
+            __syncthreads();
+            const int nk = nz - k0 < 2 * NT ? nz - k0 : 2 * NT;
+            for (int e0 = tid; e0 < nk * nl; e0 += 2 * NT) {   // (shift, l) pairs
+                cplx uv[2], yv[2];
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const int e = e0 + s * NT;
+                    const int64_t o = (int64_t)(k_lo + k0) * nl + e;
+                    uv[s] = e < nk * nl ? kp.u[o] : mk(0, 0);
+                    yv[s] = e < nk * nl ? kp.y[o] : mk(0, 0);
+                }
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const int e = e0 + s * NT;
+                    if (e >= nk * nl) continue;
+                    const int kk = e / nl, l = e - kk * nl;
+                    if (!ss.act[kk]) continue;
+                    const int64_t o = (int64_t)(k_lo + k0) * nl + e;
+                    const cplx uu = cadd(cmul(ss.g[l], ss.ip[kk]), cmul(ss.bk[kk], uv[s]));
+                    kp.u[o] = uu;
+                    kp.y[o] = cfma(ss.ak[kk], uu, yv[s]);
+                }
+            }
+        }
+    }
+    // block reduction: survivor count + argmin |pi_{n+1}|
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && (bi < 0 || ov < best || (ov == best && oi < bi))) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { ss.rc[warp] = cnt; ss.rd[warp] = best; ss.ri[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+        int cc = 0, i = -1;
+        double b = 0.0;
+        for (int w = 0; w < nw; ++w) {
+            cc += ss.rc[w];
+            const int oi = ss.ri[w];
+            const double ov = ss.rd[w];
+            if (oi >= 0 && (i < 0 || ov < b || (ov == b && oi < i))) { b = ov; i = oi; }
+        }
+        AminPart p;
+        p.a2 = b;
+        p.idx = i < 0 ? -1 : k_lo + i;
+        p.cnt = cc;
+        p.f = i < 0 ? mk(1, 0) : nxt[i];          // written by this CTA above
+        p.fp = i < 0 ? mk(1, 0) : cmul(cur[i], bc);
+        kp.amin_part[agent] = p;
     }
 }
 

@@ -11,10 +11,15 @@
 
 namespace sk {
 
-int update_blocks(int64_t M, int nl, int full) {
+int shift_agents(int nz) {
+    int a = (nz + kThreads - 1) / kThreads;   // ~one shift per agent thread
+    return a < 1 ? 1 : (a > 8 ? 8 : a);
+}
+
+int update_blocks(int64_t M, int nl, int full, int nz) {
     const int R = full ? 1 : (nl <= 4 ? 2 : 1);
     int64_t b = (M + (int64_t)kThreads * R - 1) / ((int64_t)kThreads * R);
-    const int64_t cap = 148 * 4;
+    const int64_t cap = 148 * 4 - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
@@ -51,14 +56,19 @@ __global__ void __launch_bounds__(kThreads) init_kernel(KParams kp, const cplx *
 template <int NLMAX, bool BICG, bool FULL, int R>
 __global__ void __launch_bounds__(kThreads, FULL ? 2 : 4)
 update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
-    extern __shared__ cplx dyn[];  // FULL: coef[3 * n_act], then act list (int32)
+    extern __shared__ cplx dyn[];  // FULL: coef[3 nz], flags[nz], list[nz]
+    __shared__ ShiftScratch ss;
     DevState *st = kp.st;
     if (st->status != ST_ITERATING) return;
-    if (blockIdx.x == 0) {          // shift agent (a4 + a6), beside the streaming CTAs
-        shift_step(kp);
+    if (blockIdx.x < kp.n_agents) {   // shift agents (a4 + a6 + pending a8), beside the streaming CTAs
+        if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 5);
+        shift_step(kp, ss, blockIdx.x);
+        __syncthreads();
+        if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 6);
         return;
     }
-    const int wb = blockIdx.x - 1, nwb = gridDim.x - 1;
+    if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 7);
+    const int wb = blockIdx.x - kp.n_agents, nwb = gridDim.x - kp.n_agents;
     const int64_t ns = st->n_started;            // seed step of iteration n ran: ns = n + 1
     const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);
     const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);
@@ -69,26 +79,62 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
     const cplx a_cur = st->a_cur, a_q = st->a_q, a_prev = st->a_prev;
     const cplx ac_cur = cconj(a_cur), ac_q = cconj(a_q), ac_prev = cconj(a_prev);
     int nact = 0;
-    cplx *coef = dyn;
-    int *act = nullptr;
+    cplx *coef = dyn;      // FULL: [3 nz] coefficients, dense by shift index
+    int *act = nullptr;    // FULL: compacted list of the shifts streamed this iteration
     if (FULL) {
-        // every streaming CTA evaluates the coefficients of the active shifts itself (the same
-        // arithmetic as the shift agent, so bit-identical): p^k = sr_n r_stored / pi_n^k + ...
-        nact = *kp.n_act;
-        act = (int *)(dyn + 3 * kp.nz);
+        // Every streaming CTA evaluates the pending retirement test and the coefficients of
+        // the active shifts itself — the same arithmetic as the shift agent, so identical
+        // decisions and bit-identical values: p^k = sr_n r_stored / pi_n^k + beta^k p^k.
+        const int nz = kp.nz;
+        int *flag = (int *)(dyn + 3 * nz);
+        act = flag + nz;
         const int64_t n = st->n;
-        const cplx *cur = kp.pibuf + (size_t)(n % 3) * kp.nz;
-        const cplx *prv = kp.pibuf + (size_t)((n + 2) % 3) * kp.nz;
+        const cplx *cur = kp.pibuf + (size_t)(n % 3) * nz;
+        const cplx *prv = kp.pibuf + (size_t)((n + 2) % 3) * nz;
+        const cplx bc = st->bscale[n % 3], bp = st->bscale[(n + 2) % 3];
+        const bool lz = st->lz_pending != 0 && st->lz_iter == n;
+        const double lz_nu = st->lz_nu, tol = st->tol;
         const cplx alpha = st->alpha, beta = st->beta, c = st->c, zs = st->zs, sr = st->sr_it;
-        for (int j = threadIdx.x; j < nact; j += blockDim.x) {
-            const int k = kp.act_list[j];
-            const ShiftCoef sc = shift_coef(cur[k], prv[k], kp.z[k], zs, alpha, beta, c, n);
-            act[j] = k;
-            coef[3 * j] = cmul(sr, sc.ipik);
-            coef[3 * j + 1] = sc.bk;
-            coef[3 * j + 2] = sc.ak;
+        for (int k = threadIdx.x; k < nz; k += blockDim.x) {
+            bool on = kp.active[k] != 0;
+            const cplx pik = cmul(cur[k], bc), piok = cmul(prv[k], bp);
+            if (on && lz) {
+                double rk;
+                if (retire_test(lz_nu, pik, tol, rk)) on = false;
+            }
+            flag[k] = on;
+            if (on) {
+                const ShiftCoef sc = shift_coef(pik, piok, kp.z[k], zs, alpha, beta, c, n);
+                coef[3 * k] = cmul(sr, sc.ipik);
+                coef[3 * k + 1] = sc.bk;
+                coef[3 * k + 2] = sc.ak;
+            }
         }
         __syncthreads();
+        // ascending compaction of the flags (warp ballots + a warp scan of the warp counts)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int base = 0; base < nz; base += blockDim.x) {
+            const int k = base + threadIdx.x;
+            const int f = k < nz ? flag[k] : 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) ss.ri[warp] = __popc(bal);
+            __syncthreads();
+            if (warp == 0) {
+                const int v = lane < nw ? ss.ri[lane] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (lane < nw) ss.rc[lane] = incl - v;
+                if (lane == 31) ss.ri[31] = incl;   // (nw <= 8: slot 31 is free)
+            }
+            __syncthreads();
+            if (f) act[nact + ss.rc[warp] + __popc(bal & ((1u << lane) - 1u))] = k;
+            nact += ss.ri[31];
+            __syncthreads();
+        }
     }
     cplx acc[2 + NLMAX];
 #pragma unroll
@@ -146,19 +192,21 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
 #pragma unroll
                     for (int uu = 0; uu < 4; ++uu) {
                         const int64_t off = (int64_t)act[j + uu] * M + i;
-                        cplx pn = cmul(coef[3 * (j + uu)], r0);
-                        pn = cfma(coef[3 * (j + uu) + 1], pk[uu], pn);
+                        const int kk = act[j + uu];
+                        cplx pn = cmul(coef[3 * kk], r0);
+                        pn = cfma(coef[3 * kk + 1], pk[uu], pn);
                         stg_cs(kp.p + off, pn);
-                        stg_cs(kp.x + off, cfma(coef[3 * (j + uu) + 2], pn, xk[uu]));
+                        stg_cs(kp.x + off, cfma(coef[3 * kk + 2], pn, xk[uu]));
                     }
                 }
                 for (; j < nact; ++j) {
                     const int64_t off = (int64_t)act[j] * M + i;
                     const cplx pk = ldg_cs(kp.p + off), xk = ldg_cs(kp.x + off);
-                    cplx pn = cmul(coef[3 * j], r0);
-                    pn = cfma(coef[3 * j + 1], pk, pn);
+                    const int kk = act[j];
+                    cplx pn = cmul(coef[3 * kk], r0);
+                    pn = cfma(coef[3 * kk + 1], pk, pn);
                     stg_cs(kp.p + off, pn);
-                    stg_cs(kp.x + off, cfma(coef[3 * j + 2], pn, xk));
+                    stg_cs(kp.x + off, cfma(coef[3 * kk + 2], pn, xk));
                 }
             }
         }
@@ -170,18 +218,19 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
         for (int j = 0; j < 2 + NLMAX; ++j)
             if (j < 2 + kp.nl) kp.part_u[(int64_t)wb * (2 + kp.nl) + j] = acc[j];
     }
+    if (blockIdx.x == gridDim.x - 1) dbg_stamp(kp.dbg_ts, 8);
 }
 
 template <int NLMAX, bool BICG, bool FULL>
 static cudaError_t launch_update_t(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
     constexpr int R = FULL ? 1 : (NLMAX <= 4 ? 2 : 1);   // must match update_blocks()
-    const size_t shm = FULL ? (size_t)kp.nz * (3 * sizeof(cplx) + sizeof(int)) : 0;
+    const size_t shm = FULL ? (size_t)kp.nz * (3 * sizeof(cplx) + 2 * sizeof(int)) : 0;
     if (FULL && shm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(update_kernel<NLMAX, BICG, FULL, R>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
         if (e != cudaSuccess) return e;
     }
-    update_kernel<NLMAX, BICG, FULL, R><<<kp.nblk_upd + 1, kThreads, shm, s>>>(kp, q, qt);
+    update_kernel<NLMAX, BICG, FULL, R><<<kp.nblk_upd + kp.n_agents, kThreads, shm, s>>>(kp, q, qt);
     return cudaGetLastError();
 }
 

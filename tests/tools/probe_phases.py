@@ -1,0 +1,19 @@
+"""Phase stamps (ns, relative to the first SpMV worker CTA) of one iteration."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+os.environ["SHIFTK_DEBUG_TS"] = "1"
+import torch
+import synth
+from paper_2001_08707_b200.device import to_device, make_solver
+p = synth.make_problem(sys.argv[1] if len(sys.argv) > 1 else "c2")
+g = make_solver(to_device(p))
+g.run(20)
+names = {0: "spmv_worker1_start", 1: "agent_start", 2: "finish_done", 3: "last_cta", 4: "seed_done",
+         5: "shift_agent_start", 6: "shift_done", 7: "upd_worker1_start", 8: "upd_lastcta_end",
+         9: "fin_reduced", 10: "fin_shiftloop", 11: "fin_switched", 12: "fin_compacted"}
+for i in range(4):
+    g.enqueue(1)
+    torch.cuda.synchronize()
+    ts = g.debug_timestamps()
+    t0 = ts[0]
+    print({names[k]: int(ts[k] - t0) for k in range(13)})
