@@ -51,6 +51,17 @@ def lib():
         L.or_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _c128p, _c128p,
                                 ctypes.c_int64, _c128p, ctypes.c_int, ctypes.c_double,
                                 ctypes.c_int64, ctypes.c_int]
+        L.or_create_subset.restype = ctypes.c_void_p
+        L.or_create_subset.argtypes = L.or_create.argtypes + [ctypes.c_void_p]
+        class _C(ctypes.Structure):
+            _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
+        L._C = _C
+        L.or_heisenberg_row.restype = _C
+        L.or_heisenberg_row.argtypes = [ctypes.c_int, ctypes.c_double, _c128p, ctypes.c_int64]
+        L.or_csr_real_row.restype = _C
+        L.or_csr_real_row.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64]
+        L.or_csr_cplx_row.restype = _C
+        L.or_csr_cplx_row.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64]
         L.or_destroy.argtypes = [ctypes.c_void_p]
         L.or_update.restype = ctypes.c_int
         L.or_update.argtypes = [ctypes.c_void_p, _c128p, _c128p]
@@ -102,6 +113,22 @@ def csr_apply(op: dict, r: np.ndarray) -> np.ndarray:
     return q
 
 
+def apply_rows(op: dict, r: np.ndarray, rows) -> np.ndarray:
+    """q_s = (H r)_s for the listed rows only (same arithmetic as apply_op)."""
+    r = np.ascontiguousarray(r, dtype=np.complex128)
+    out = np.empty(len(rows), dtype=np.complex128)
+    L_ = lib()
+    for j, s in enumerate(rows):
+        if op["kind"] == "heisenberg":
+            v = L_.or_heisenberg_row(op["L"], op["J"], _ptr(r), int(s))
+        elif op["kind"] == "csr_real":
+            v = L_.or_csr_real_row(_ptr(op["row_ptr"]), _ptr(op["col"]), _ptr(op["val"]), _ptr(r), int(s))
+        else:
+            v = L_.or_csr_cplx_row(_ptr(op["row_ptr"]), _ptr(op["col"]), _ptr(op["val"]), _ptr(r), int(s))
+        out[j] = complex(v.re, v.im)
+    return out
+
+
 def apply_op(op: dict, r: np.ndarray) -> np.ndarray:
     """q = H r with the oracle's own operator code."""
     if op["kind"] == "heisenberg":
@@ -116,7 +143,8 @@ class Oracle:
     P:L517-523, Alg. 1)."""
 
     def __init__(self, method: str, b: np.ndarray, z: np.ndarray, *, left: Optional[np.ndarray] = None,
-                 full_x: bool = False, tol: float = 1e-10, itermax: int = 10000, flags: int = 0):
+                 full_x: bool = False, tol: float = 1e-10, itermax: int = 10000, flags: int = 0,
+                 keep: Optional[np.ndarray] = None):
         self.method = COCG if method == "cocg" else BICG
         self.b = np.ascontiguousarray(b, dtype=np.complex128)
         self.z = np.ascontiguousarray(z, dtype=np.complex128)
@@ -124,9 +152,11 @@ class Oracle:
         self.left = None if left is None else np.ascontiguousarray(left, dtype=np.complex128)
         self.nleft = 1 if left is None else self.left.shape[0]
         self.full_x = bool(full_x)
-        self._h = lib().or_create(self.method, self.M, self.nz, _ptr(self.z), _ptr(self.b),
-                                  self.nleft, 0 if self.left is None else _ptr(self.left),
-                                  int(self.full_x), float(tol), int(itermax), int(flags))
+        self._keep = None if keep is None else np.ascontiguousarray(keep, dtype=np.uint8)
+        self._h = lib().or_create_subset(self.method, self.M, self.nz, _ptr(self.z), _ptr(self.b),
+                                         self.nleft, 0 if self.left is None else _ptr(self.left),
+                                         int(self.full_x), float(tol), int(itermax), int(flags),
+                                         0 if self._keep is None else _ptr(self._keep))
         if not self._h:
             raise ValueError("oracle init rejected its arguments")
 
@@ -213,7 +243,10 @@ class Oracle:
     def solution(self, k: int) -> np.ndarray:
         if not self.full_x:
             raise ValueError("full x not stored")
-        return _view(lib().or_x(self._h, k), self.M, np.complex128)
+        addr = lib().or_x(self._h, k)
+        if not addr:
+            raise ValueError(f"x of shift {k} not carried (keep mask)")
+        return _view(addr, self.M, np.complex128)
 
     def scalars(self) -> dict:
         out = np.zeros(6, dtype=np.complex128)

@@ -67,7 +67,8 @@ typedef struct {
     double *res;
     int64_t *retired_at;
     cplx *g, *u, *y;           /* g: [nleft]; u, y: [nz][nleft] */
-    cplx *p, *x;               /* [nz][M] when full */
+    cplx *p, *x;               /* [nz][M] when full (only shifts with keep[k]) */
+    unsigned char *keep;       /* full mode: which shifts carry x, p (all by default) */
     cplx alpha_prev, rho_prev;
     cplx alpha, beta, rho, w;  /* last iteration's seed scalars (for inspection) */
     int64_t n, nswitch, nspmv;
@@ -113,9 +114,22 @@ static void *xcalloc(size_t n, size_t sz) { return calloc(n ? n : 1, sz); }
 void or_destroy(or_state *st);
 
 /* left == NULL  ->  a = b (one left vector equal to b). */
+or_state *or_create_subset(int method, int64_t M, int64_t nz, const cplx *z, const cplx *b,
+                           int64_t nleft, const cplx *left, int full, double tol, int64_t itermax,
+                           int flags, const unsigned char *keep);
+
 or_state *or_create(int method, int64_t M, int64_t nz, const cplx *z, const cplx *b,
                     int64_t nleft, const cplx *left, int full, double tol, int64_t itermax,
                     int flags) {
+    return or_create_subset(method, M, nz, z, b, nleft, left, full, tol, itermax, flags, NULL);
+}
+
+/* Full mode with x, p stored only for the shifts with keep[k] != 0 (NULL = all).  The scalar
+   recurrences, retirement and seed switching still run over every shift, and they never read
+   x or p, so the iterates of the carried shifts are exactly those of a run carrying all. */
+or_state *or_create_subset(int method, int64_t M, int64_t nz, const cplx *z, const cplx *b,
+                           int64_t nleft, const cplx *left, int full, double tol, int64_t itermax,
+                           int flags, const unsigned char *keep) {
     if (M <= 0 || nz <= 0 || (method != OR_COCG && method != OR_BICG) || tol <= 0 || itermax < 1)
         return NULL;
     or_state *st = (or_state *)xcalloc(1, sizeof(or_state));
@@ -141,9 +155,16 @@ or_state *or_create(int method, int64_t M, int64_t nz, const cplx *z, const cplx
     st->g = (cplx *)xcalloc(st->nleft, sizeof(cplx));
     st->u = (cplx *)xcalloc(nz * st->nleft, sizeof(cplx));
     st->y = (cplx *)xcalloc(nz * st->nleft, sizeof(cplx));
+    st->keep = (unsigned char *)xcalloc(nz, 1);
+    int64_t nkeep = 0;
+    for (int64_t k = 0; k < nz; ++k) {
+        st->keep[k] = keep ? (keep[k] != 0) : 1;
+        nkeep += st->keep[k];
+    }
     if (full) {
-        st->p = (cplx *)xcalloc((size_t)(nz * M), sizeof(cplx));
-        st->x = (cplx *)xcalloc((size_t)(nz * M), sizeof(cplx));
+        /* x, p rows of the kept shifts only, addressed through slot[] */
+        st->p = (cplx *)xcalloc((size_t)(nkeep * M), sizeof(cplx));
+        st->x = (cplx *)xcalloc((size_t)(nkeep * M), sizeof(cplx));
         if (!st->p || !st->x) { or_destroy(st); return NULL; }
     }
     memcpy(st->b, b, M * sizeof(cplx));
@@ -171,7 +192,7 @@ void or_destroy(or_state *st) {
     free(st->b); free(st->left); free(st->r); free(st->r_old); free(st->tmp);
     free(st->t); free(st->t_old); free(st->z); free(st->pi); free(st->pi_old); free(st->pi_new);
     free(st->active); free(st->res); free(st->retired_at); free(st->g); free(st->u); free(st->y);
-    free(st->p); free(st->x);
+    free(st->p); free(st->x); free(st->keep);
     free(st);
 }
 
@@ -215,8 +236,10 @@ int or_update(or_state *st, const cplx *q, const cplx *qt) {
             *u = st->g[l] / st->pi[k] + bk * (*u);
             *y = *y + ak * (*u);
         }
-        if (st->full) {
-            cplx *p = st->p + k * M, *x = st->x + k * M;
+        if (st->full && st->keep[k]) {
+            int64_t slot = 0;
+            for (int64_t j = 0; j < k; ++j) slot += st->keep[j];
+            cplx *p = st->p + slot * M, *x = st->x + slot * M;
             for (int64_t i = 0; i < M; ++i) {
                 p[i] = st->r[i] / st->pi[k] + bk * p[i];
                 x[i] = x[i] + ak * p[i];
@@ -332,6 +355,37 @@ void or_csr_cplx_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, co
     }
 }
 
+/* One output element of the operators (for sampled parity at sizes where a full product is
+   too slow): q_s = sum_j H_sj r_j, same arithmetic as the full products above. */
+cplx or_heisenberg_row(int L, double J, const cplx *r, int64_t s) {
+    cplx acc = 0;
+    for (int i = 0; i < L; ++i) {
+        int j = (i + 1) % L;
+        int bi = (int)((s >> i) & 1), bj = (int)((s >> j) & 1);
+        if (bi == bj) {
+            acc += 0.25 * J * r[s];
+        } else {
+            acc += -0.25 * J * r[s];
+            acc += 0.5 * J * r[s ^ (((int64_t)1 << i) | ((int64_t)1 << j))];
+        }
+    }
+    return acc;
+}
+
+cplx or_csr_real_row(const int64_t *row_ptr, const int32_t *col, const double *val, const cplx *r,
+                     int64_t i) {
+    cplx acc = 0;
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
+    return acc;
+}
+
+cplx or_csr_cplx_row(const int64_t *row_ptr, const int32_t *col, const cplx *val, const cplx *r,
+                     int64_t i) {
+    cplx acc = 0;
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
+    return acc;
+}
+
 /* ------------------------------------------------------------------ accessors */
 
 int or_status(const or_state *st) { return st->status; }
@@ -348,7 +402,12 @@ const double *or_res(const or_state *st) { return st->res; }
 const unsigned char *or_active(const or_state *st) { return st->active; }
 const int64_t *or_retired_at(const or_state *st) { return st->retired_at; }
 const cplx *or_y(const or_state *st) { return st->y; }
-const cplx *or_x(const or_state *st, int64_t k) { return st->full ? st->x + k * st->M : NULL; }
+const cplx *or_x(const or_state *st, int64_t k) {
+    if (!st->full || !st->keep[k]) return NULL;
+    int64_t slot = 0;
+    for (int64_t j = 0; j < k; ++j) slot += st->keep[j];
+    return st->x + slot * st->M;
+}
 void or_scalars(const or_state *st, cplx *out /* [6] */) {
     out[0] = st->alpha; out[1] = st->beta; out[2] = st->rho; out[3] = st->w;
     out[4] = st->zs; out[5] = st->alpha_prev;
