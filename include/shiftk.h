@@ -116,16 +116,30 @@ typedef struct {
     int64_t itermax;         /* iteration budget >= 1 (maxloops)                    */
 } sk_params;
 
-/* Multi-GPU placement.  world == 1: single GPU, nccl_id ignored.  world > 1: rows are sharded
-   (this rank passes its own rows of b, left vectors and CSR), dot products are summed with
-   NCCL all-reduce; nccl_id is the 128-byte ncclUniqueId broadcast by the caller. */
+typedef struct sk_group sk_group;
+
+/* Multi-GPU placement (the paper's optional MPI).  world == 1: one GPU.
+   world > 1: the vector rows are sharded — rank g owns global rows [g M_local, (g+1) M_local),
+   M_local = M / world a power of two (for the Heisenberg chain: the top log2(world) spin bits
+   select the rank), and passes its own rows of b, of the left vectors and of the CSR (global
+   column ids).  Dot products are all-reduced (NCCL, or a loopback group); the SpMV reads the
+   rows it needs from the other ranks IN PLACE through peer memory (CUDA IPC mappings over
+   NVLink) — the operator exchange is fused into the SpMV's loads.
+   Two ways to run world > 1:
+     * one process per GPU (NCCL): group == NULL.  sk_init, then exchange sk_ipc_handle()
+       (64 B per rank, all-gathered by the caller) and one sk_nccl_unique_id() (128 B, from
+       rank 0), then sk_connect().  All calls are collective in iteration order.
+     * loopback group (tests on one GPU): group from sk_group_create(world); sk_init every rank
+       with that group, sk_group_connect(), then sk_group_update / sk_group_run drive all ranks.
+   Contexts of world > 1 refuse sk_update / sk_run until connected. */
 typedef struct {
     int32_t rank;
     int32_t world;
-    int32_t device;          /* CUDA device ordinal                                            */
+    int32_t device;          /* CUDA device ordinal (ignored for a loopback group)             */
     int32_t reserved;
-    const void *nccl_id;     /* 128 bytes, or NULL when world == 1                              */
+    const void *nccl_id;     /* unused (see sk_connect); kept for layout stability              */
     void *stream;            /* cudaStream_t to use, or NULL (library creates one)             */
+    sk_group *group;         /* loopback group, or NULL                                         */
 } sk_dist;
 
 /* Current seed/shift coefficients (the quantities the paper logs in TriDiagComp.dat). */
@@ -225,6 +239,24 @@ int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
 /* Diagnostics: %globaltimer stamps (ns) written by instrumented kernels (16 slots; see
    csrc/steps.cuh).  Requires the environment variable SHIFTK_DEBUG_TS at sk_init. */
 int sk_debug_timestamps(sk_ctx *ctx, int64_t *out16);
+
+/* ---- multi-rank setup (see sk_dist) ---- */
+/* CUDA IPC handle (64 bytes) of this context's device arena, for the other ranks. */
+int sk_ipc_handle(sk_ctx *ctx, void *out64);
+/* A fresh ncclUniqueId (128 bytes); call on one rank and broadcast. */
+int sk_nccl_unique_id(void *out128);
+/* Map every other rank's arena (handles: [world][64] from sk_ipc_handle, in rank order), join
+   the NCCL communicator and finish the initialisation (global rho_0, ||b||, P b).  Collective. */
+int sk_connect(sk_ctx *ctx, const void *handles, const void *nccl_id);
+/* Loopback group of `world` virtual ranks on one device (all share one stream). */
+int sk_group_create(sk_group **out, int32_t world, int32_t device);
+/* After sk_init of every rank with this group: wire the ranks and finish initialisation. */
+int sk_group_connect(sk_group *group);
+/* One iteration / up to max_iters iterations of every rank (status of the group). */
+int sk_group_update(sk_group *group, int32_t *status);
+int sk_group_run(sk_group *group, int64_t max_iters, int32_t *status);
+/* Release the group (every member context must be finalized first). */
+int sk_group_destroy(sk_group **group);
 
 /* Library version / build info string (never NULL). */
 const char *sk_version(void);

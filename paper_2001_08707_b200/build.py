@@ -12,9 +12,19 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libshiftk.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+def _nccl_dir():
+    try:
+        import nvidia.nccl
+        return list(nvidia.nccl.__path__)[0]
+    except Exception:   # headers are needed at build time only; the library is dlopen'ed
+        return "/usr"
+
+
+NCCL_DIR = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-shared", "-I" + os.path.join(ROOT, "include"),
-         "--expt-relaxed-constexpr"]
+         "-I" + os.path.join(NCCL_DIR, "include"), "--expt-relaxed-constexpr",
+         '-DSHIFTK_NCCL_DEFAULT="' + os.path.join(NCCL_DIR, "lib", "libnccl.so.2") + '"', "-ldl"]
 
 
 def sources():

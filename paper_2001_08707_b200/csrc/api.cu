@@ -2,6 +2,8 @@
 // enqueueing (single step / CUDA-graph captured loop), getters.  Every step of the method runs in
 // the kernels of kernels.cu; this file only allocates, enqueues and copies.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
@@ -13,6 +15,8 @@
 
 #include "../../include/shiftk.h"
 #include "kernels.cuh"
+
+using sk::LoopbackPtrs;
 
 
 static thread_local std::string g_err = "no error";
@@ -28,6 +32,50 @@ static int fail(int code, const std::string &msg) {
         if (e_ != cudaSuccess)                                                                   \
             return fail(SK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));            \
     } while (0)
+
+// ---- NCCL, loaded on first multi-rank use (the torch-bundled libnccl.so.2; no link-time
+// dependency, so single-GPU users never need it) ----------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void *h = nullptr;
+    if (const char *p = getenv("SHIFTK_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen(SHIFTK_NCCL_DEFAULT, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.getErrorString;
+    return api;
+}
+
+#define NK(call)                                                                                 \
+    do {                                                                                         \
+        ncclResult_t e_ = (call);                                                                \
+        if (e_ != ncclSuccess)                                                                   \
+            return fail(SK_ENCCL, std::string(#call) + ": " + nccl().getErrorString(e_));         \
+    } while (0)
+
+struct sk_group {   // single-GPU loopback group: `world` virtual ranks in one process
+    int world = 0, device = 0;
+    cudaStream_t stream = nullptr;
+    std::vector<sk_ctx *> members;
+    bool connected = false;
+};
 
 struct sk_ctx {
     int device = 0;
@@ -58,6 +106,14 @@ struct sk_ctx {
     size_t ev_used = 0;
     int64_t prof_iters = 0;
     double prof_ms[3] = {0, 0, 0};
+    // multi-rank
+    int world = 1, rank = 0;
+    sk_group *group = nullptr;      // loopback group (single GPU), or
+    ncclComm_t comm = nullptr;      // NCCL communicator (one process per GPU)
+    bool connected = true;          // false until sk_connect / sk_group_connect
+    void *arena = nullptr;
+    size_t arena_bytes = 0;
+    std::vector<void *> peer_bases; // opened IPC mappings of the other ranks' arenas
 };
 
 static cudaError_t prof_mark(sk_ctx *c) {
@@ -89,6 +145,10 @@ static void destroy(sk_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->graph) cudaGraphExecDestroy(c->graph);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (void *p : c->peer_bases)
+        if (p) cudaIpcCloseMemHandle(p);
+    if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
+    if (c->group && c->rank < (int)c->group->members.size()) c->group->members[c->rank] = nullptr;
     for (void *p : c->allocs) cudaFree(p);
     if (c->st_host) cudaFreeHost(c->st_host);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -96,11 +156,13 @@ static void destroy(sk_ctx *c) {
 }
 
 // --------------------------------------------------------------------------- enqueue helpers
-// One iteration = two launches:
+// One iteration (world == 1) = two launches:
 //   SpMV (+ finish of the previous iteration in CTA 0, + seed scalars in the last CTA)
-//   update (+ per-shift recurrences in CTA 0).
-static int enqueue_iteration(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc) {
-    sk::SpmvArgs a{};
+//   update (+ per-shift recurrences in the agent CTAs).
+// world > 1: SpMV (peer loads through the shard tables; last CTA -> this rank's w) ->
+//   all-reduce(w) -> seed kernel -> update (last CTA -> this rank's dots) -> all-reduce(dots).
+static int enqueue_phase_a(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc, sk::SpmvArgs &a) {
+    a = sk::SpmvArgs{};
     a.st = c->st;
     for (int i = 0; i < 3; ++i) { a.r[i] = c->kp.r[i]; a.t[i] = c->kp.t[i]; }
     a.q = q_rc ? (cplx *)q_rc : c->kp.q;
@@ -117,12 +179,70 @@ static int enqueue_iteration(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc) {
         CK(sk::launch_csr(a, c->kp, c->op.row_ptr, c->op.col, c->op.val, c->op.kind == SK_OP_CSR_CPLX,
                           c->avg_nnz, c->stream));
     CK(prof_mark(c));
+    if (!c->capturing) c->launches += 1;
+    return SK_OK;
+}
+
+static int enqueue_phase_b(sk_ctx *c, const sk::SpmvArgs &a) {
     CK(sk::launch_update(c->kp, a.q, a.qt, c->stream));
     CK(prof_mark(c));
-    if (!c->capturing) c->launches += 2;
+    if (!c->capturing) c->launches += 1;
     c->host_started += 1;
     c->pending_host = true;
     return SK_OK;
+}
+
+static int nccl_allreduce(sk_ctx *c, const cplx *src, cplx *dst, int ncplx) {
+    NK(nccl().allReduce(src, dst, 2 * (size_t)ncplx, ncclDouble, ncclSum, c->comm, c->stream));
+    return SK_OK;
+}
+
+static int enqueue_iteration(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc) {
+    if (!c->connected) return fail(SK_ESTATE, "multi-rank context not connected (sk_connect)");
+    if (c->group) return fail(SK_ESTATE, "loopback group member: use sk_group_update / sk_group_run");
+    sk::SpmvArgs a;
+    int rc;
+    if ((rc = enqueue_phase_a(c, q_rc, qt_rc, a)) != SK_OK) return rc;
+    if (c->world > 1) {
+        if ((rc = nccl_allreduce(c, c->kp.wloc, c->kp.wsum, 1)) != SK_OK) return rc;
+        CK(sk::launch_seed(c->kp, c->stream));
+        if (!c->capturing) c->launches += 1;
+    }
+    if ((rc = enqueue_phase_b(c, a)) != SK_OK) return rc;
+    if (c->world > 1 && (rc = nccl_allreduce(c, c->kp.uloc, c->kp.usum, 2 + c->nl)) != SK_OK) return rc;
+    return SK_OK;
+}
+
+// Loopback all-reduce over the members of a single-GPU group (deterministic, rank order).
+static int group_allreduce(sk_group *g, bool dots) {
+    LoopbackPtrs p{};
+    int n = 0;
+    for (int r = 0; r < g->world; ++r) {
+        sk_ctx *m = g->members[r];
+        p.src[r] = dots ? m->kp.uloc : m->kp.wloc;
+        p.dst[r] = dots ? m->kp.usum : m->kp.wsum;
+        n = dots ? 2 + m->nl : 1;
+    }
+    sk_ctx *m0 = g->members[0];
+    cudaError_t e = sk::launch_loopback_allreduce(p, g->world, n, g->stream);
+    if (e != cudaSuccess) return fail(SK_ECUDA, std::string("loopback all-reduce: ") + cudaGetErrorString(e));
+    m0->launches += 1;
+    return SK_OK;
+}
+
+static int group_iteration(sk_group *g) {
+    std::vector<sk::SpmvArgs> a(g->world);
+    int rc;
+    for (int r = 0; r < g->world; ++r)
+        if ((rc = enqueue_phase_a(g->members[r], nullptr, nullptr, a[r])) != SK_OK) return rc;
+    if ((rc = group_allreduce(g, false)) != SK_OK) return rc;
+    for (int r = 0; r < g->world; ++r) {
+        CK(sk::launch_seed(g->members[r]->kp, g->stream));
+        g->members[r]->launches += 1;
+    }
+    for (int r = 0; r < g->world; ++r)
+        if ((rc = enqueue_phase_b(g->members[r], a[r])) != SK_OK) return rc;
+    return group_allreduce(g, true);
 }
 
 static int enqueue_finish(sk_ctx *c) {
@@ -151,8 +271,13 @@ const char *sk_version(void) {
 int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dist *d) {
     if (!out || !H || !p) return fail(SK_EINVAL, "null argument");
     *out = nullptr;
-    const int world = d ? d->world : 1;
-    if (world != 1) return fail(SK_EUNSUPPORTED, "world > 1 is not supported by this build");
+    const int world = d ? (d->world < 1 ? 1 : d->world) : 1;
+    const int rank = d ? d->rank : 0;
+    sk_group *group = d ? (sk_group *)d->group : nullptr;
+    if (world > sk::kMaxWorld) return fail(SK_EUNSUPPORTED, "world > 64");
+    if (rank < 0 || rank >= world) return fail(SK_EINVAL, "rank out of range");
+    if (group && (group->world != world || group->members[rank] != nullptr))
+        return fail(SK_EINVAL, "group size mismatch or rank already initialised");
     if (p->method != SK_COCG && p->method != SK_BICG) return fail(SK_EINVAL, "method");
     if (p->n_shift < 1 || !p->z) return fail(SK_EINVAL, "n_shift >= 1 and z required");
     if (!(p->tol > 0)) return fail(SK_EINVAL, "tol must be > 0");
@@ -163,16 +288,22 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     if (p->n_left > 32) return fail(SK_EUNSUPPORTED, "n_left > 32");
     if (p->n_shift > (1 << 20)) return fail(SK_EUNSUPPORTED, "n_shift > 2^20");
     const int64_t M = H->M_local > 0 ? H->M_local : H->M;
+    if (world > 1) {   // rows [rank * M_local, (rank + 1) * M_local), M_local a power of two
+        if (M * world != H->M || (M & (M - 1)) != 0 || H->row_begin != (int64_t)rank * M)
+            return fail(SK_EINVAL, "multi-rank: need M = world * M_local, M_local a power of two, "
+                                   "row_begin = rank * M_local");
+        if (H->kind == SK_OP_RC) return fail(SK_EUNSUPPORTED, "reverse communication with world > 1");
+    }
     switch (H->kind) {
         case SK_OP_HEISENBERG:
-            if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L) || M != H->M)
-                return fail(SK_EINVAL, "Heisenberg: need 1 <= L <= 34 and M = M_local = 2^L");
+            if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L) || (world == 1 && M != H->M))
+                return fail(SK_EINVAL, "Heisenberg: need 1 <= L <= 34, M = 2^L");
             break;
         case SK_OP_CSR_REAL:
         case SK_OP_CSR_CPLX:
             if (!H->row_ptr || !H->col || !H->val || M < 1 || H->nnz < 0)
                 return fail(SK_EINVAL, "CSR arrays / sizes");
-            if (M != H->M) return fail(SK_EINVAL, "CSR: M_local must equal M when world == 1");
+            if (world == 1 && M != H->M) return fail(SK_EINVAL, "CSR: M_local must equal M when world == 1");
             if (H->kind == SK_OP_CSR_CPLX && p->method == SK_COCG)
                 return fail(SK_EUNSUPPORTED,
                             "COCG needs a complex-symmetric z I - H: use BiCG for complex "
@@ -187,7 +318,11 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
 
     sk_ctx *c = new (std::nothrow) sk_ctx();
     if (!c) return fail(SK_ENOMEM, "host allocation");
-    c->device = d ? d->device : 0;
+    c->device = group ? group->device : (d ? d->device : 0);
+    c->world = world;
+    c->rank = rank;
+    c->group = group;
+    c->connected = world == 1;
     c->op = *H;
     c->method = p->method;
     c->full = p->full_x ? 1 : 0;
@@ -203,7 +338,9 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     auto bail = [&](int code) { destroy(c); return code; };
 
     if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(SK_ECUDA, "cudaSetDevice"));
-    if (d && d->stream) {
+    if (group) {
+        c->stream = group->stream;   // every member of a loopback group shares one stream
+    } else if (d && d->stream) {
         c->stream = (cudaStream_t)d->stream;
     } else {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -224,6 +361,11 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M) : sk::stream_blocks(M);
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
     kp.n_agents = sk::shift_agents(c->nz);
+    kp.world = world;
+    kp.rank = rank;
+    kp.row0 = world > 1 ? (int64_t)rank * M : 0;
+    kp.lloc_bits = 0;
+    while ((int64_t(1) << kp.lloc_bits) < M) ++kp.lloc_bits;
     const size_t vb = (size_t)M * sizeof(cplx);
 
     // One device arena for everything the context owns (one cudaMalloc / cudaFree); every
@@ -256,6 +398,15 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&kp.y, sizeof(cplx) * c->nz * c->nl);
         add(&kp.g, sizeof(cplx) * c->nl);
         if (getenv("SHIFTK_DEBUG_TS")) add(&kp.dbg_ts, sizeof(int64_t) * 16);
+        if (world > 1) {
+            add(&kp.wloc, sizeof(cplx));
+            add(&kp.wsum, sizeof(cplx));
+            add(&kp.uloc, sizeof(cplx) * (2 + c->nl));
+            add(&kp.usum, sizeof(cplx) * (2 + c->nl));
+            add(&kp.ticket_u, sizeof(uint32_t));
+            add(&kp.shard_r, sizeof(cplx *) * 3 * world);
+            add(&kp.shard_t, sizeof(cplx *) * 3 * world);
+        }
         if (!c->a_is_b && p->left_mem != SK_MEM_DEVICE) add(&c->left_owned, vb * c->nl);
         if (c->full) {
             add(&kp.p, vb * c->nz);
@@ -265,6 +416,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         for (auto &it : items) total += (it.bytes + 255) & ~size_t(255);
         void *arena = nullptr;
         if ((rc = dalloc(c, &arena, total)) != SK_OK) return bail(rc);
+        c->arena = arena;
+        c->arena_bytes = total;
         size_t off = 0;
         for (auto &it : items) {
             *it.p = (char *)arena + off;
@@ -313,10 +466,160 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         if (cudaStreamSynchronize(c->stream)) return bail(fail(SK_ECUDA, "sync"));
     }
     if (sk::launch_init(kp, c->b, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init kernel"));
+    if (world > 1) {   // the global rho_0, ||b||, P b need the other ranks: finished at connect
+        if (sk::launch_reduce_local(kp, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init reduce"));
+        if (group) group->members[rank] = c;
+        *out = c;
+        return SK_OK;
+    }
     if (sk::launch_scalar(kp, sk::PH_INIT, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init scalar"));
     if ((rc = read_state(c)) != SK_OK) return bail(rc);
     if (!(c->st_host->nu > 0)) return bail(fail(SK_EINVAL, "||b|| must be > 0"));
     *out = c;
+    return SK_OK;
+}
+
+// Shard tables: entry [b * world + g] = rank g's r[b] (t[b]), given every rank's arena base.
+static int write_shard_tables(sk_ctx *c, const std::vector<char *> &bases) {
+    std::vector<const cplx *> tr(3 * c->world), tt(3 * c->world);
+    char *mine = (char *)c->arena;
+    for (int b = 0; b < 3; ++b)
+        for (int g = 0; g < c->world; ++g) {
+            tr[b * c->world + g] = (const cplx *)(bases[g] + ((char *)c->kp.r[b] - mine));
+            tt[b * c->world + g] = c->kp.bicg ? (const cplx *)(bases[g] + ((char *)c->kp.t[b] - mine)) : nullptr;
+        }
+    CK(cudaMemcpyAsync((void *)c->kp.shard_r, tr.data(), sizeof(cplx *) * tr.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync((void *)c->kp.shard_t, tt.data(), sizeof(cplx *) * tt.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+static int finish_init(sk_ctx *c) {
+    CK(sk::launch_scalar(c->kp, sk::PH_INIT, c->stream));
+    int rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    if (!(c->st_host->nu > 0)) return fail(SK_EINVAL, "||b|| must be > 0");
+    c->connected = true;
+    return SK_OK;
+}
+
+int sk_ipc_handle(sk_ctx *c, void *out64) {
+    if (!c || !out64) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    cudaIpcMemHandle_t h;
+    CK(cudaSetDevice(c->device));
+    CK(cudaIpcGetMemHandle(&h, c->arena));
+    memcpy(out64, &h, sizeof(h));
+    return SK_OK;
+}
+
+int sk_nccl_unique_id(void *out128) {
+    if (!out128) return fail(SK_EINVAL, "null argument");
+    if (!nccl().ok) return fail(SK_ENCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    NK(nccl().getUniqueId(&id));
+    memcpy(out128, &id, sizeof(id));
+    return SK_OK;
+}
+
+int sk_connect(sk_ctx *c, const void *handles, const void *nccl_id) {
+    if (!c || !handles || !nccl_id) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (c->world == 1 || c->group || c->connected) return fail(SK_ESTATE, "not an unconnected NCCL-mode context");
+    if (!nccl().ok) return fail(SK_ENCCL, "libnccl.so.2 not loadable");
+    CK(cudaSetDevice(c->device));
+    std::vector<char *> bases(c->world);
+    c->peer_bases.assign(c->world, nullptr);
+    for (int g = 0; g < c->world; ++g) {
+        if (g == c->rank) { bases[g] = (char *)c->arena; continue; }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const char *)handles + 64 * g, sizeof(h));
+        void *p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->peer_bases[g] = p;
+        bases[g] = (char *)p;
+    }
+    int rc;
+    if ((rc = write_shard_tables(c, bases)) != SK_OK) return rc;
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    NK(nccl().commInitRank(&c->comm, c->world, id, c->rank));
+    if ((rc = nccl_allreduce(c, c->kp.uloc, c->kp.usum, 2 + c->nl)) != SK_OK) return rc;
+    return finish_init(c);
+}
+
+int sk_group_create(sk_group **out, int32_t world, int32_t device) {
+    if (!out || world < 1 || world > sk::kMaxWorld) return fail(SK_EINVAL, "group size");
+    sk_group *g = new (std::nothrow) sk_group();
+    if (!g) return fail(SK_ENOMEM, "host allocation");
+    g->world = world;
+    g->device = device;
+    g->members.assign(world, nullptr);
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete g;
+        return fail(SK_ECUDA, "group stream");
+    }
+    *out = g;
+    return SK_OK;
+}
+
+int sk_group_destroy(sk_group **pg) {
+    if (!pg || !*pg) return fail(SK_ESTATE, "null group");
+    sk_group *g = *pg;
+    for (sk_ctx *m : g->members)
+        if (m) return fail(SK_ESTATE, "finalize every member context first");
+    cudaStreamSynchronize(g->stream);
+    cudaStreamDestroy(g->stream);
+    delete g;
+    *pg = nullptr;
+    return SK_OK;
+}
+
+int sk_group_connect(sk_group *g) {
+    if (!g) return fail(SK_ESTATE, "null group");
+    if (g->connected) return fail(SK_ESTATE, "group already connected");
+    for (sk_ctx *m : g->members)
+        if (!m) return fail(SK_ESTATE, "every rank of the group must be initialised first");
+    std::vector<char *> bases(g->world);
+    for (int r = 0; r < g->world; ++r) bases[r] = (char *)g->members[r]->arena;
+    int rc;
+    for (sk_ctx *m : g->members)
+        if ((rc = write_shard_tables(m, bases)) != SK_OK) return rc;
+    if ((rc = group_allreduce(g, true)) != SK_OK) return rc;
+    for (sk_ctx *m : g->members)
+        if ((rc = finish_init(m)) != SK_OK) return rc;
+    g->connected = true;
+    return SK_OK;
+}
+
+int sk_group_update(sk_group *g, int32_t *status) {
+    if (!g || !g->connected) return fail(SK_ESTATE, "group not connected");
+    CK(cudaSetDevice(g->device));
+    int rc;
+    for (sk_ctx *m : g->members)
+        if ((rc = enqueue_finish(m)) != SK_OK) return rc;
+    if ((rc = group_iteration(g)) != SK_OK) return rc;
+    for (sk_ctx *m : g->members)
+        if ((rc = enqueue_finish(m)) != SK_OK) return rc;
+    if ((rc = read_state(g->members[0])) != SK_OK) return rc;
+    if (status) *status = g->members[0]->st_host->status;
+    return SK_OK;
+}
+
+int sk_group_run(sk_group *g, int64_t max_iters, int32_t *status) {
+    if (!g || !g->connected) return fail(SK_ESTATE, "group not connected");
+    CK(cudaSetDevice(g->device));
+    int rc;
+    if ((rc = read_state(g->members[0])) != SK_OK) return rc;
+    int64_t done = 0;
+    while (done < max_iters && g->members[0]->st_host->status == SK_ITERATING) {
+        const int64_t chunk = max_iters - done < 64 ? max_iters - done : 64;
+        for (int64_t i = 0; i < chunk; ++i)
+            if ((rc = group_iteration(g)) != SK_OK) return rc;
+        done += chunk;
+        for (sk_ctx *m : g->members)
+            if ((rc = enqueue_finish(m)) != SK_OK) return rc;
+        if ((rc = read_state(g->members[0])) != SK_OK) return rc;
+    }
+    if (status) *status = g->members[0]->st_host->status;
     return SK_OK;
 }
 

@@ -143,6 +143,18 @@ struct KParams {
     uint32_t *ticket;    // [1] last-CTA detection in the SpMV kernel (reset by the last CTA)
     int32_t n_agents;    // shift-agent CTAs of the update kernel (each a slice of the shifts)
     struct AminPart *amin_part;   // [n_agents] per-agent argmin |pi_{n+1}| and survivor count
+    // ---- multi-rank (world > 1): this rank owns global rows [row0, row0 + M); every rank's r
+    // (and r~) buffers are reachable through shard tables (NVLink peer mappings of the other
+    // ranks' arenas, or the other contexts of a single-GPU loopback group).
+    int32_t world, rank;
+    int32_t lloc_bits;           // log2(M): M (rows per rank) is a power of two when world > 1
+    int32_t pad_;
+    int64_t row0;
+    const cplx *const *shard_r;  // device [3 * world]: shard_r[b * world + g] = rank g's r[b]
+    const cplx *const *shard_t;  // device [3 * world] (BiCG shadow)
+    cplx *wloc, *wsum;           // [1] this rank's / all-reduced SpMV dot  (world > 1)
+    cplx *uloc, *usum;           // [2 + nl] this rank's / all-reduced update dots (world > 1)
+    uint32_t *ticket_u;          // [1] last-CTA detection in the update kernel (world > 1)
 };
 
 // Per shift-agent result: argmin over its slice of |pi_{n+1}|^2 (lowest index on ties).

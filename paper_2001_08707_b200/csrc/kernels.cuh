@@ -44,4 +44,14 @@ cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cuda
 enum : int { PH_INIT = 1, PH_FINISH = 2 };
 cudaError_t launch_scalar(const KParams &kp, int phase, cudaStream_t s);
 
+// ---- multi-rank (world > 1) -----------------------------------------------------------------
+constexpr int kMaxWorld = 64;
+struct LoopbackPtrs {
+    const cplx *src[kMaxWorld];
+    cplx *dst[kMaxWorld];
+};
+cudaError_t launch_seed(const KParams &kp, cudaStream_t s);            // seed step on wsum
+cudaError_t launch_reduce_local(const KParams &kp, cudaStream_t s);    // init partials -> uloc
+cudaError_t launch_loopback_allreduce(const LoopbackPtrs &p, int world, int n, cudaStream_t s);
+
 }  // namespace sk

@@ -21,11 +21,35 @@ int stream_blocks(int64_t M) {
 }
 
 int heisenberg_blocks(int L, int64_t M) {
-    if (L > kTileBits && L <= 34) {
+    if (L > kTileBits && L <= 34 && M >= (int64_t(1) << kTileBits)) {
         const int64_t ntiles = M >> kTileBits;
         return (int)(ntiles < (int64_t)kMaxBlocks ? ntiles : (int64_t)kMaxBlocks);
     }
     return stream_blocks(M);
+}
+
+// View of one rotating r buffer as the GLOBAL vector: this rank's rows are local; with
+// world > 1 every other rank's rows are reached through the shard table (peer memory over
+// NVLink, or the other contexts of a loopback group) — the exchange of the operator is fused
+// into the SpMV's own loads.
+struct RView {
+    const cplx *loc;
+    const cplx *const *tab;   // [world] for this buffer index, or null (world <= 1)
+    int64_t row0;
+    int lloc, world;
+    __device__ __forceinline__ const cplx *at(uint64_t g) const {
+        if (world <= 1) return loc + (int64_t)(g - (uint64_t)row0);
+        return tab[g >> lloc] + (g & ((1ull << lloc) - 1ull));
+    }
+};
+__device__ __forceinline__ RView rview(const cplx *loc, const cplx *const *shard, int buf, const KParams &kp) {
+    RView v;
+    v.loc = loc;
+    v.world = kp.world;
+    v.tab = (kp.world > 1 && shard) ? shard + (size_t)buf * kp.world : nullptr;
+    v.row0 = kp.world > 1 ? kp.row0 : 0;
+    v.lloc = kp.lloc_bits;
+    return v;
 }
 
 // Common prologue/epilogue of the solver-mode SpMV kernels.  Returns false when the kernel
@@ -64,6 +88,14 @@ __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParams &kp, 
     if (!last) return;
     dbg_stamp(kp.dbg_ts, 3);                                       // last CTA arrives
     __threadfence();
+    if (kp.world > 1) {   // this rank's w only: the all-reduce and the seed step follow
+        reduce_columns(a.part_w, gridDim.x - 1, 1, 1, sc);
+        if (threadIdx.x == 0) {
+            kp.wloc[0] = sc.col[0];
+            *kp.ticket = 0u;
+        }
+        return;
+    }
     state_load_nosync(sc.S, kp.st);
     reduce_columns(a.part_w, gridDim.x - 1, 1, 1, sc);   // (its barriers publish sc.S)
     if (threadIdx.x == 0) {
@@ -89,14 +121,16 @@ __global__ void __launch_bounds__(kThreads) heisenberg_kernel(SpmvArgs a, KParam
     if (!spmv_enter(a, agent, buf, sc, kp)) return;
     const cplx *__restrict__ r = pick3(a.r, buf);
     const cplx *__restrict__ t = pick3(a.t, buf);
+    const RView rv = rview(r, kp.shard_r, buf, kp), tv = rview(t, kp.shard_t, buf, kp);
     const double qJ = 0.25 * J, hJ = 0.5 * J;
     const int64_t M = a.M;
+    const uint64_t row0 = (uint64_t)rv.row0;
     const int off = a.st ? 1 : 0;
     cplx w = mk(0.0, 0.0);
     if (!agent) {
         for (int64_t s = (int64_t)(blockIdx.x - off) * blockDim.x + threadIdx.x; s < M;
              s += (int64_t)(gridDim.x - off) * blockDim.x) {
-            const uint64_t us = (uint64_t)s;
+            const uint64_t us = row0 + (uint64_t)s;   // global basis state
             const uint64_t x = us ^ ((us >> 1) | ((us & 1ull) << (L - 1)));
             const double d = qJ * (double)(L - 2 * __popcll(x));
             const cplx rs = r[s];
@@ -107,11 +141,11 @@ __global__ void __launch_bounds__(kThreads) heisenberg_kernel(SpmvArgs a, KParam
                 if ((x >> i) & 1ull) {
                     const int j = (i + 1 == L) ? 0 : i + 1;
                     const uint64_t s2 = us ^ ((1ull << i) | (1ull << j));
-                    const cplx v = r[s2];
+                    const cplx v = *rv.at(s2);
                     q.x = fma(hJ, v.x, q.x);
                     q.y = fma(hJ, v.y, q.y);
                     if (NRHS == 2) {
-                        const cplx vt = t[s2];
+                        const cplx vt = *tv.at(s2);
                         qt.x = fma(hJ, vt.x, qt.x);
                         qt.y = fma(hJ, vt.y, qt.y);
                     }
@@ -152,33 +186,41 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
     static_assert(PER * kThreads == TS, "tile must be a multiple of the CTA size");
     const cplx *__restrict__ r = pick3(a.r, buf);
     const cplx *__restrict__ t = pick3(a.t, buf);
+    // global view of r (and r~): with world > 1 partner tiles on other ranks are read in place
+    // through peer memory; every partner tile below is resolved once per tile (its shard is
+    // uniform over the tile).
+    const RView rv = rview(r, kp.shard_r, buf, kp), tv = rview(t, kp.shard_t, buf, kp);
     const double qJ = 0.25 * J, hJ = 0.5 * J;
     const int64_t ntiles = a.M >> T;
     const int tid = threadIdx.x;
     const int off = a.st ? 1 : 0;
     cplx w = mk(0.0, 0.0);
     for (int64_t ti = (int64_t)blockIdx.x - off; !agent && ti < ntiles; ti += gridDim.x - off) {
-        const U base = (U)(ti << T);
+        const int64_t lbase = ti << T;                  // local row of the tile
+        const U base = (U)(rv.row0 + lbase);            // global basis state of the tile
         __syncthreads();   // previous tile's shared-memory reads are done
         cplx q[PER], qt[NRHS == 2 ? PER : 1];
         {
             cplx v0[PER], v1[PER], v2[PER], t0[NRHS == 2 ? PER : 1], t1[NRHS == 2 ? PER : 1],
                 t2[NRHS == 2 ? PER : 1];
             const U tb = (base >> T) & (U)1, hb = (base >> (L - 1)) & (U)1;
+            // partner tiles: bond (T-1, T) flips bit T (and bit T-1 inside the tile); the
+            // periodic bond (L-1, 0) flips bit L-1 (and bit 0 inside the tile)
+            const cplx *p1 = rv.at(base ^ ((U)1 << T)), *p2 = rv.at(base ^ ((U)1 << (L - 1)));
+            const cplx *p1t = nullptr, *p2t = nullptr;
+            if (NRHS == 2) { p1t = tv.at(base ^ ((U)1 << T)); p2t = tv.at(base ^ ((U)1 << (L - 1))); }
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const int ls = tid + k * kThreads;
-                const U s = base + (U)ls;
-                v0[k] = r[s];
-                if (NRHS == 2) t0[k] = t[s];
+                v0[k] = r[lbase + ls];
+                if (NRHS == 2) t0[k] = t[lbase + ls];
                 const bool on1 = ((U)((ls >> (T - 1)) & 1) ^ tb) != 0;    // bond (T-1, T)
-                const U s1 = s ^ ((U)3 << (T - 1));
-                v1[k] = on1 ? r[s1] : mk(0.0, 0.0);
-                if (NRHS == 2) t1[k] = on1 ? t[s1] : mk(0.0, 0.0);
+                const int l1 = ls ^ (1 << (T - 1));
+                v1[k] = on1 ? p1[l1] : mk(0.0, 0.0);
+                if (NRHS == 2) t1[k] = on1 ? p1t[l1] : mk(0.0, 0.0);
                 const bool on2 = ((U)(ls & 1) ^ hb) != 0;                 // bond (L-1, 0)
-                const U s2 = s ^ (((U)1 << (L - 1)) | (U)1);
-                v2[k] = on2 ? r[s2] : mk(0.0, 0.0);
-                if (NRHS == 2) t2[k] = on2 ? t[s2] : mk(0.0, 0.0);
+                v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
+                if (NRHS == 2) t2[k] = on2 ? p2t[ls ^ 1] : mk(0.0, 0.0);
             }
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
@@ -214,11 +256,13 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 cplx v[NB][PER], vt[NB][NRHS == 2 ? PER : 1];
 #pragma unroll
                 for (int m = 0; m < NB; ++m) {
-                    const U pb = base ^ ((U)3 << (bi[m] < 0 ? 0 : bi[m]));
+                    const U pb = base ^ ((U)3 << (bi[m] < 0 ? T : bi[m]));
+                    const cplx *pt = rv.at(pb);
+                    const cplx *ptt = NRHS == 2 ? tv.at(pb) : nullptr;
 #pragma unroll
                     for (int k = 0; k < PER; ++k) {
-                        v[m][k] = bi[m] >= 0 ? r[pb + (U)(tid + k * kThreads)] : mk(0.0, 0.0);
-                        if (NRHS == 2) vt[m][k] = bi[m] >= 0 ? t[pb + (U)(tid + k * kThreads)] : mk(0.0, 0.0);
+                        v[m][k] = bi[m] >= 0 ? pt[tid + k * kThreads] : mk(0.0, 0.0);
+                        if (NRHS == 2) vt[m][k] = bi[m] >= 0 ? ptt[tid + k * kThreads] : mk(0.0, 0.0);
                     }
                 }
 #pragma unroll
@@ -250,9 +294,9 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                     }
                 }
             }
-            a.q[s] = q[k];
+            a.q[lbase + ls] = q[k];
             if (NRHS == 2) {
-                a.qt[s] = qt[k];
+                a.qt[lbase + ls] = qt[k];
                 w = cfma_conj(tile[TS + ls], q[k], w);
             } else {
                 w = cfma(tile[ls], q[k], w);
@@ -283,7 +327,7 @@ static cudaError_t launch_tiled(const SpmvArgs &a, const KParams &kp, double J, 
 cudaError_t launch_heisenberg(const SpmvArgs &a, const KParams &kp, int L, double J, cudaStream_t s) {
     const int workers = heisenberg_blocks(L, a.M);
     const int grid = workers + (a.st ? 1 : 0);
-    switch (L) {
+    if (a.M >= (int64_t(1) << kTileBits)) switch (L) {
 #define SK_TILED_CASE(LL) case LL: return launch_tiled<LL>(a, kp, J, grid, s);
         SK_TILED_CASE(11) SK_TILED_CASE(12) SK_TILED_CASE(13) SK_TILED_CASE(14) SK_TILED_CASE(15)
         SK_TILED_CASE(16) SK_TILED_CASE(17) SK_TILED_CASE(18) SK_TILED_CASE(19) SK_TILED_CASE(20)
@@ -311,6 +355,7 @@ csr_kernel(SpmvArgs a, KParams kp, const int64_t *__restrict__ rp, const int32_t
     if (!spmv_enter(a, agent, buf, sc, kp)) return;
     const cplx *__restrict__ r = pick3(a.r, buf);
     const cplx *__restrict__ t = pick3(a.t, buf);
+    const RView rv = rview(r, kp.shard_r, buf, kp), tv = rview(t, kp.shard_t, buf, kp);
     const int off = a.st ? 1 : 0;
     const int lane = threadIdx.x & (LPR - 1);
     const unsigned gmask = (LPR == 32) ? 0xffffffffu
@@ -322,20 +367,20 @@ csr_kernel(SpmvArgs a, KParams kp, const int64_t *__restrict__ rp, const int32_t
             const int64_t e0 = rp[i], e1 = rp[i + 1];
             cplx acc = mk(0.0, 0.0), acct = mk(0.0, 0.0);
             for (int64_t e = e0 + lane; e < e1; e += LPR) {
-                const int c = col[e];
-                const cplx rv = r[c];
+                const int c = col[e];                      // global column id
+                const cplx x = *rv.at((uint64_t)c);
                 if (CV) {
                     const cplx v = ((const cplx *)valv)[e];
-                    acc = cfma(v, rv, acc);
-                    if (NRHS == 2) acct = cfma(v, t[c], acct);
+                    acc = cfma(v, x, acc);
+                    if (NRHS == 2) acct = cfma(v, *tv.at((uint64_t)c), acct);
                 } else {
                     const double v = ((const double *)valv)[e];
-                    acc.x = fma(v, rv.x, acc.x);
-                    acc.y = fma(v, rv.y, acc.y);
+                    acc.x = fma(v, x.x, acc.x);
+                    acc.y = fma(v, x.y, acc.y);
                     if (NRHS == 2) {
-                        const cplx tv = t[c];
-                        acct.x = fma(v, tv.x, acct.x);
-                        acct.y = fma(v, tv.y, acct.y);
+                        const cplx xt = *tv.at((uint64_t)c);
+                        acct.x = fma(v, xt.x, acct.x);
+                        acct.y = fma(v, xt.y, acct.y);
                     }
                 }
             }

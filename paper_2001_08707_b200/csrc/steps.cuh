@@ -60,6 +60,12 @@ static __device__ __forceinline__ void state_store(DevState *dst, const DevState
 constexpr int kSpt = 4;             // shifts per thread per block of a step loop
 constexpr int kSmemShifts = 4096;   // shifts whose active flags fit in the scratch copy
 
+// Scratch of a column reduction.
+struct RedScratch {
+    cplx col[40];                // reduced partial columns
+    cplx red[4][32];             // per-warp partial sums (4 columns at a time)
+};
+
 // Shared scratch of the step functions (one instance per CTA that runs them).
 struct StepScratch {
     DevState S;                  // shared copy of the device state
@@ -75,8 +81,9 @@ struct StepScratch {
 // Sum columns [0, ncol) of part[nblk][stride] into sc.col — fixed order (per-thread strided
 // sum over b = tid + 4k*NT.., then warps in index order): deterministic.  Loads of 4 blocks x
 // up to 4 columns are issued before they are summed.  All threads call it; ends with a barrier.
+template <typename Scratch>
 static __device__ __forceinline__ void reduce_columns(const cplx *part, int nblk, int stride, int ncol,
-                                                      StepScratch &sc) {
+                                                      Scratch &sc) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int NT = blockDim.x;
     for (int cb = 0; cb < ncol; cb += 4) {
@@ -220,7 +227,8 @@ static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eage
     state_load_nosync(sc.S, kp.st);
     DevState *S = &sc.S;
     const int nl = kp.nl, nred = 2 + nl;
-    reduce_columns(kp.part_u, kp.nblk_upd, nred, nred, sc);   // (its barriers publish sc.S)
+    if (kp.usum) reduce_columns(kp.usum, 1, nred, nred, sc);         // all-reduced (world > 1)
+    else reduce_columns(kp.part_u, kp.nblk_upd, nred, nred, sc);   // (barriers publish sc.S)
     const int64_t m = S->n;
     const double nu = sqrt(sc.col[1].x);
     if (threadIdx.x == 0) {

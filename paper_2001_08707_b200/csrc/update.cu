@@ -219,6 +219,19 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
             if (j < 2 + kp.nl) kp.part_u[(int64_t)wb * (2 + kp.nl) + j] = acc[j];
     }
     if (blockIdx.x == gridDim.x - 1) dbg_stamp(kp.dbg_ts, 8);
+    if (kp.world > 1) {   // this rank's dots for the all-reduce: the last worker CTA sums them
+        __shared__ RedScratch rs;
+        __shared__ int last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = (atomicAdd(kp.ticket_u, 1u) == (unsigned)nwb - 1u);
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        reduce_columns(kp.part_u, nwb, 2 + kp.nl, 2 + kp.nl, rs);
+        if (threadIdx.x < 2 + kp.nl) kp.uloc[threadIdx.x] = rs.col[threadIdx.x];
+        if (threadIdx.x == 0) *kp.ticket_u = 0u;
+    }
 }
 
 template <int NLMAX, bool BICG, bool FULL>

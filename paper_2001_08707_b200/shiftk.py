@@ -28,7 +28,9 @@ ERRORS = {0: "SK_OK", -1: "SK_EINVAL", -2: "SK_ENOMEM", -3: "SK_ECUDA", -4: "SK_
 EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_run", "sk_enqueue",
            "sk_get_residual", "sk_get_projection", "sk_get_solution", "sk_get_shift_state",
            "sk_get_coefficients", "sk_finalize", "sk_apply_operator", "sk_last_error", "sk_version",
-           "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps"]
+           "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
+           "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
+           "sk_group_update", "sk_group_run", "sk_group_destroy"]
 
 
 class ShiftkError(RuntimeError):
@@ -57,7 +59,8 @@ class sk_params(ctypes.Structure):
 
 class sk_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+                ("reserved", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+                ("group", ctypes.c_void_p)]
 
 
 class sk_coeffs(ctypes.Structure):
@@ -103,6 +106,14 @@ def load(path: str = LIB_PATH):
         "sk_profile_enable": [VP, I32],
         "sk_copy_solution": [VP, I64, VP, I32],
         "sk_debug_timestamps": [VP, VP],
+        "sk_ipc_handle": [VP, VP],
+        "sk_nccl_unique_id": [VP],
+        "sk_connect": [VP, VP, VP],
+        "sk_group_create": [P(VP), I32, I32],
+        "sk_group_connect": [VP],
+        "sk_group_update": [VP, P(I32)],
+        "sk_group_run": [VP, I64, P(I32)],
+        "sk_group_destroy": [P(VP)],
         "sk_get_profile": [VP, P(sk_profile), I32],
     }
     for name, args in sig.items():
@@ -135,13 +146,15 @@ def _ptr_mem(a):
     return a.ctypes.data, MEM_HOST
 
 
-def make_operator(op: dict, M: int, dev_arrays: Optional[dict] = None) -> sk_operator:
+def make_operator(op: dict, M: int, dev_arrays: Optional[dict] = None, *, M_local: Optional[int] = None,
+                  row_begin: int = 0) -> sk_operator:
     """Build sk_operator from a synth op dict; CSR arrays must be given as device tensors in
-    ``dev_arrays`` (row_ptr int64, col int32, val float64/complex128)."""
+    ``dev_arrays`` (row_ptr int64, col int32, val float64/complex128) holding this rank's rows
+    [row_begin, row_begin + M_local) of the global M x M matrix."""
     o = sk_operator()
     o.M = M
-    o.M_local = M
-    o.row_begin = 0
+    o.M_local = M if M_local is None else M_local
+    o.row_begin = row_begin
     if op["kind"] == "heisenberg":
         o.kind, o.L, o.J = OP_HEISENBERG, int(op["L"]), float(op["J"])
     elif op["kind"] in ("csr_real", "csr_cplx"):
@@ -176,13 +189,52 @@ def apply_operator(op: sk_operator, r_dev, q_dev, stream: int = 0):
                                     ctypes.c_void_p(stream)), "sk_apply_operator")
 
 
+class Group:
+    """Loopback group: ``world`` virtual ranks on one GPU (sk_group_*)."""
+
+    def __init__(self, world: int, device: int = 0):
+        self._h = ctypes.c_void_p()
+        self.world = world
+        _check(load().sk_group_create(ctypes.byref(self._h), world, device), "sk_group_create")
+        self.members = []
+
+    def connect(self):
+        _check(load().sk_group_connect(self._h), "sk_group_connect")
+
+    def update(self) -> int:
+        st = ctypes.c_int32()
+        _check(load().sk_group_update(self._h, ctypes.byref(st)), "sk_group_update")
+        return st.value
+
+    def run(self, max_iters: int) -> int:
+        st = ctypes.c_int32()
+        _check(load().sk_group_run(self._h, max_iters, ctypes.byref(st)), "sk_group_run")
+        return st.value
+
+    def close(self):
+        for m in self.members:
+            m.finalize()
+        self.members = []
+        if self._h and self._h.value:
+            _check(load().sk_group_destroy(ctypes.byref(self._h)), "sk_group_destroy")
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_char * 128)()
+    _check(load().sk_nccl_unique_id(buf), "sk_nccl_unique_id")
+    return bytes(buf)
+
+
 class Solver:
     """One sk_ctx.  ``b``/``left`` may be numpy arrays (host; copied) or torch tensors (device:
-    b copied, left borrowed).  ``op`` is an sk_operator (keep its device arrays alive)."""
+    b copied, left borrowed).  ``op`` is an sk_operator (keep its device arrays alive).
+    Multi-rank: ``rank``/``world`` with either ``group`` (loopback) or, for one process per
+    GPU, a later :meth:`connect`."""
 
     def __init__(self, op: sk_operator, method: str, b, z: np.ndarray, *, left=None,
                  full_x: bool = False, tol: float = 1e-10, itermax: int = 10000, flags: int = 0,
-                 device: int = 0, stream: int = 0):
+                 device: int = 0, stream: int = 0, rank: int = 0, world: int = 1,
+                 group: Optional[Group] = None):
         L = load()
         self._keep = [op, b, left]
         self.z = np.ascontiguousarray(z, dtype=np.complex128)
@@ -204,12 +256,24 @@ class Solver:
         p.tol = tol
         p.itermax = itermax
         d = sk_dist()
-        d.rank, d.world, d.device = 0, 1, device
+        d.rank, d.world, d.device = rank, world, device
         d.nccl_id, d.stream = None, stream or None
+        d.group = group._h.value if group is not None else None
         self._h = ctypes.c_void_p()
         _check(L.sk_init(ctypes.byref(self._h), ctypes.byref(op), ctypes.byref(p), ctypes.byref(d)),
                "sk_init")
         self.M = int(op.M_local)
+        if group is not None:
+            group.members.append(self)
+
+    # -- multi-rank (one process per GPU) ---------------------------------------------------
+    def ipc_handle(self) -> bytes:
+        buf = (ctypes.c_char * 64)()
+        _check(load().sk_ipc_handle(self._h, buf), "sk_ipc_handle")
+        return bytes(buf)
+
+    def connect(self, handles: bytes, nccl_id: bytes):
+        _check(load().sk_connect(self._h, handles, nccl_id), "sk_connect")
 
     # -- iteration ---------------------------------------------------------------------
     def update(self) -> int:

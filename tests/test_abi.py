@@ -52,7 +52,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(shiftk.sk_cplx) == 16
     assert ctypes.sizeof(shiftk.sk_operator) == 4 + 4 + 8 + 8 * 4 + 8 * 3
     assert ctypes.sizeof(shiftk.sk_params) == 4 + 4 + 8 + 8 + 8 + 4 + 4 + 8 + 8 + 4 + 4 + 8 + 8
-    assert ctypes.sizeof(shiftk.sk_dist) == 16 + 16
+    assert ctypes.sizeof(shiftk.sk_dist) == 16 + 16 + 8
 
 
 def test_sm100a_cubin_inside():
