@@ -163,8 +163,8 @@ def run_reference(args, problem):
               f"of the full-size workload (M={problem.M}, N_z={problem.n_shift})")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-            "data": "synthetic", "config": config_dict(problem, world),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "config": config_dict(problem, 1),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -173,7 +173,10 @@ def run_reference(args, problem):
 def config_dict(problem, world):
     c = {"workload": f"{problem.name}: {synth.CONFIGS[problem.name.split('[')[0]]['desc']}",
          "M": problem.M, "n_shift": problem.n_shift, "n_left": problem.n_left,
-         "method": problem.method, "full_x": problem.full_x, "parallelism": f"replicas{world}",
+         "method": problem.method, "full_x": problem.full_x,
+         "parallelism": "single GPU" if world == 1 else
+         f"rows sharded over {world} GPUs (top spin bits / contiguous row blocks); dots by NCCL "
+         f"all-reduce; other ranks' rows read in place over NVLink (CUDA IPC)",
          "l2": "flushed before every timed step (256 MiB write, outside the events)"}
     return c
 
@@ -207,11 +210,18 @@ def main():
     from paper_2001_08707_b200 import shiftk
     from paper_2001_08707_b200.device import to_device
 
-    dp = to_device(problem, f"cuda:{local}")
     stream = torch.cuda.Stream()
+    if world == 1:
+        dp = to_device(problem, f"cuda:{local}")
+        sl = None
+    else:   # this rank's rows; the global problem is the same on every rank (strong scaling)
+        from paper_2001_08707_b200 import dist as skdist
+        dp, sl = skdist.to_device_slice(problem, world, rank, f"cuda:{local}")
     solver = shiftk.Solver(dp.op, problem.method, dp.b, problem.z, left=dp.left,
                            full_x=problem.full_x, tol=problem.tol, itermax=10 ** 9,
-                           device=local, stream=stream.cuda_stream)
+                           device=local, stream=stream.cuda_stream, rank=rank, world=world)
+    if world > 1:
+        skdist.connect(solver)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     solver.profile_enable(True)
     with torch.cuda.stream(stream):
@@ -243,25 +253,25 @@ def main():
         t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = problem.n_shift * args.steps * world / (total_ms * 1e-3)
+    value = problem.n_shift * args.steps / (total_ms * 1e-3)   # one global problem (strong scaling)
 
     # roofline of the dominant kernel (per launch: algorithmic bytes / mean device duration)
     peak, peak_src = measured_peaks()
     kernels = {"spmv": prof["ms_spmv"], "update": prof["ms_update"]}
     dom = max(kernels, key=kernels.get)
     per_launch_ms = kernels[dom] / max(prof["iterations"], 1)
-    alg_bytes = bytes_per_row(problem, dom) * problem.M
+    alg_bytes = bytes_per_row(problem, dom) * problem.M / world   # this rank's rows
     achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(f"{problem.name}:{dom}")
-    iter_bytes = (bytes_per_row(problem, "spmv") + bytes_per_row(problem, "update")) * problem.M
+    iter_bytes = (bytes_per_row(problem, "spmv") + bytes_per_row(problem, "update")) * problem.M / world
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": config_dict(problem, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -279,14 +289,19 @@ def main():
 
     # end-to-end through the public API with HOST buffers (pinned b in, results out)
     if not args.no_e2e:
-        b_host = torch.from_numpy(problem.b).pin_memory()
-        left_host = None if problem.left is None else torch.from_numpy(problem.left).pin_memory()
+        src_b = problem.b if sl is None else sl.b
+        src_left = problem.left if sl is None else sl.left
+        b_host = torch.from_numpy(src_b).pin_memory()
+        left_host = None if src_left is None else torch.from_numpy(src_left).pin_memory()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         s2 = shiftk.Solver(dp.op, problem.method, b_host, problem.z, left=left_host,
-                           full_x=problem.full_x, tol=problem.tol, itermax=10 ** 9, device=local)
+                           full_x=problem.full_x, tol=problem.tol, itermax=10 ** 9, device=local,
+                           rank=rank, world=world)
+        if world > 1:
+            skdist.connect(s2)
         s2.run(args.steps, poll_every=max(args.steps, 1))
         y = s2.projections()
         res = s2.residuals()
@@ -296,9 +311,9 @@ def main():
             t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        h2d = problem.b.nbytes + problem.z.nbytes + (0 if problem.left is None else problem.left.nbytes)
+        h2d = src_b.nbytes + problem.z.nbytes + (0 if src_left is None else src_left.nbytes)
         d2h = y.nbytes + res.nbytes
-        line["e2e"] = {"value": problem.n_shift * args.steps * world / e2e_s, "unit": UNIT,
+        line["e2e"] = {"value": problem.n_shift * args.steps / e2e_s, "unit": UNIT,
                        "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                        "note": "sk_init(host b) + sk_run(K) + sk_get_projection/residual + finalize"}
 
