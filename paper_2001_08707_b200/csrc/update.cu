@@ -17,7 +17,7 @@ int shift_agents(int nz) {
 }
 
 int update_blocks(int64_t M, int nl, int full, int nz) {
-    const int R = full ? 1 : (nl <= 4 ? 2 : 1);
+    const int R = full ? 1 : (nl <= 4 ? 2 : 1);   // (the N_left > 4 kernel uses 256-row chunks)
     int64_t b = (M + (int64_t)kThreads * R - 1) / ((int64_t)kThreads * R);
     const int64_t cap = 148 * 4 - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
     if (b > cap) b = cap;
@@ -234,6 +234,106 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
     }
 }
 
+// Projection-heavy variant (N_left > 4, projections only; C4 has 32 left vectors = 512 B/row,
+// 63% of its bytes).  Holding N_left accumulators per thread would spill, so a CTA works on
+// 256-row chunks: every thread forms r_{n+1} (+ shadow) for one row and parks it in shared
+// memory; then warp w owns left vectors l = w, w+8, w+16, w+24 and streams a_l over the chunk
+// (8 rows per lane, eight coalesced 16-byte loads in flight) into 4 per-lane accumulators.
+template <bool BICG>
+__global__ void __launch_bounds__(kThreads, 4)
+update_proj_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
+    __shared__ ShiftScratch ss;
+    __shared__ cplx rtile[kThreads];
+    __shared__ cplx scratch[4 * (kThreads / 32)];
+    __shared__ cplx lsum[32][1];
+    DevState *st = kp.st;
+    if (st->status != ST_ITERATING) return;
+    if (blockIdx.x < kp.n_agents) {   // shift agents, beside the streaming CTAs
+        shift_step(kp, ss, blockIdx.x);
+        return;
+    }
+    const int wb = blockIdx.x - kp.n_agents, nwb = gridDim.x - kp.n_agents;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ns = st->n_started;
+    const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);
+    const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);
+    cplx *__restrict__ rn_ = pick3(kp.r, ns);
+    const cplx *__restrict__ tc_ = pick3(kp.t, ns + 2);
+    const cplx *__restrict__ tp_ = pick3(kp.t, ns + 1);
+    cplx *__restrict__ tn_ = pick3(kp.t, ns);
+    const cplx a_cur = st->a_cur, a_q = st->a_q, a_prev = st->a_prev;
+    const cplx ac_cur = cconj(a_cur), ac_q = cconj(a_q), ac_prev = cconj(a_prev);
+    const int64_t M = kp.M;
+    const int nl = kp.nl;
+    cplx rho = mk(0, 0), nu = mk(0, 0);
+    cplx pa[4] = {mk(0, 0), mk(0, 0), mk(0, 0), mk(0, 0)};   // l = warp + 8 j
+    for (int64_t base = (int64_t)wb * kThreads; base < M; base += (int64_t)nwb * kThreads) {
+        const int64_t i = base + tid;
+        cplx rn = mk(0, 0);
+        if (i < M) {
+            const cplx rc = ldg_cs(rc_ + i), rp = ldg_cs(rp_ + i), qi = ldg_cs(q + i);
+            rn = cmul(a_cur, rc);
+            rn = cfma(a_q, qi, rn);
+            rn = cfma(a_prev, rp, rn);
+            rn_[i] = rn;
+            if (BICG) {
+                const cplx tc = ldg_cs(tc_ + i), tp = ldg_cs(tp_ + i), qti = ldg_cs(qt + i);
+                cplx tn = cmul(ac_cur, tc);
+                tn = cfma(ac_q, qti, tn);
+                tn = cfma(ac_prev, tp, tn);
+                tn_[i] = tn;
+                rho = cfma_conj(tn, rn, rho);
+            } else {
+                rho = cfma(rn, rn, rho);
+            }
+            nu.x = fma(rn.x, rn.x, fma(rn.y, rn.y, nu.x));
+        }
+        __syncthreads();   // previous chunk's tile reads done
+        rtile[tid] = rn;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int l = warp + 8 * j;
+            if (l >= nl) break;
+            const cplx *al = kp.left + (int64_t)l * M + base;
+            cplx av[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int row = lane + 32 * m;
+                av[m] = (base + row < M) ? ldg_cs(al + row) : mk(0, 0);
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) pa[j] = cfma_conj(av[m], rtile[lane + 32 * m], pa[j]);
+        }
+    }
+    // CTA partials: rho, ||r||^2 (block sum) and a_l^dagger r (per-warp sums)
+    cplx v2[2] = {rho, nu};
+    block_sum<2>(v2, scratch);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const cplx s = warp_sum(pa[j]);
+        const int l = warp + 8 * j;
+        if (lane == 0 && l < nl) lsum[l][0] = s;   // (one warp owns each l)
+    }
+    __syncthreads();
+    cplx *dst = kp.part_u + (int64_t)wb * (2 + nl);
+    if (tid == 0) { dst[0] = v2[0]; dst[1] = v2[1]; }
+    if (tid < nl) dst[2 + tid] = lsum[tid][0];
+    if (kp.world > 1) {   // this rank's dots for the all-reduce: the last worker CTA sums them
+        __shared__ RedScratch rs;
+        __shared__ int last;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) last = (atomicAdd(kp.ticket_u, 1u) == (unsigned)nwb - 1u);
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        reduce_columns(kp.part_u, nwb, 2 + nl, 2 + nl, rs);
+        if (tid < 2 + nl) kp.uloc[tid] = rs.col[tid];
+        if (tid == 0) *kp.ticket_u = 0u;
+    }
+}
+
 template <int NLMAX, bool BICG, bool FULL>
 static cudaError_t launch_update_t(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
     constexpr int R = FULL ? 1 : (NLMAX <= 4 ? 2 : 1);   // must match update_blocks()
@@ -257,6 +357,11 @@ static cudaError_t launch_update_nl(const KParams &kp, const cplx *q, const cplx
 }
 
 cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
+    if (kp.nl > 4 && !kp.full) {
+        if (kp.bicg) update_proj_kernel<true><<<kp.nblk_upd + kp.n_agents, kThreads, 0, s>>>(kp, q, qt);
+        else update_proj_kernel<false><<<kp.nblk_upd + kp.n_agents, kThreads, 0, s>>>(kp, q, qt);
+        return cudaGetLastError();
+    }
     if (kp.nl <= 1) return launch_update_nl<1>(kp, q, qt, s);
     if (kp.nl <= 4) return launch_update_nl<4>(kp, q, qt, s);
     if (kp.nl <= 8) return launch_update_nl<8>(kp, q, qt, s);
