@@ -358,7 +358,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.full = c->full;
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
-    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M) : sk::stream_blocks(M);
+    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M)
+                   : (H->kind == SK_OP_RC ? sk::stream_blocks(M) : sk::csr_blocks(M));
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
@@ -384,7 +385,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
             if (kp.bicg) add(&kp.qt, vb);
         }
         add(&c->b, vb);
-        add(&kp.part_w, sizeof(cplx) * sk::kMaxBlocks);
+        add(&kp.part_w, sizeof(cplx) * sk::kMaxSpmvBlocks);
         add(&kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
         add(&zdev, sizeof(cplx) * c->nz);
         add(&kp.pibuf, sizeof(cplx) * 3 * c->nz);

@@ -7,10 +7,12 @@ namespace sk {
 constexpr int kThreads = 256;          // streaming kernels
 constexpr int kScalarThreads = 1024;   // the single-CTA init / finish kernel
 constexpr int kMaxBlocks = 148 * 8;    // grid cap for grid-stride streaming kernels
+constexpr int kMaxSpmvBlocks = 148 * 32;   // grid cap (= partial slots) of the SpMV kernels
 constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
 
 int stream_blocks(int64_t M);
 int heisenberg_blocks(int L, int64_t M);        // worker CTAs (= partials) of the Heisenberg SpMV
+int csr_blocks(int64_t M);                      // worker CTAs (= partials) of the CSR SpMV
 int update_blocks(int64_t M, int nl, int full, int nz); // worker CTAs (= partials) of the update
 int shift_agents(int nz);                        // shift-agent CTAs of the update
 

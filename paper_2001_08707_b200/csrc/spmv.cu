@@ -6,6 +6,7 @@
 //   * the last CTA to finish (ticket) reduces the w partials in CTA order and computes the seed
 //     scalars of this iteration (steps.cuh seed_step).
 // Operators: on-the-fly S=1/2 Heisenberg chain (generated as in P:L508) and CSR.
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -407,6 +408,67 @@ csr_kernel(SpmvArgs a, KParams kp, const int64_t *__restrict__ rp, const int32_t
     spmv_exit(a, kp, agent, w, sc);
 }
 
+// Row-per-thread CSR variant: each thread owns whole rows and issues the loads of four entries
+// (column ids, values, then the four gathers) before their FMAs, so a warp keeps 32 rows'
+// dependent chains (row_ptr -> col -> r[col]) in flight instead of 32/LPR.
+template <bool CV, int NRHS>
+__global__ void __launch_bounds__(kThreads)
+csr_row_kernel(SpmvArgs a, KParams kp, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+               const void *__restrict__ valv) {
+    __shared__ StepScratch sc;
+    bool agent;
+    int buf;
+    if (!spmv_enter(a, agent, buf, sc, kp)) return;
+    const cplx *__restrict__ r = pick3(a.r, buf);
+    const cplx *__restrict__ t = pick3(a.t, buf);
+    const RView rv = rview(r, kp.shard_r, buf, kp), tv = rview(t, kp.shard_t, buf, kp);
+    const int off = a.st ? 1 : 0;
+    cplx w = mk(0.0, 0.0);
+    if (!agent) {
+        for (int64_t i = (int64_t)(blockIdx.x - off) * blockDim.x + threadIdx.x; i < a.M;
+             i += (int64_t)(gridDim.x - off) * blockDim.x) {
+            const int64_t e0 = rp[i], e1 = rp[i + 1];
+            cplx acc = mk(0.0, 0.0), acct = mk(0.0, 0.0);
+            for (int64_t e = e0; e < e1; e += 4) {
+                int c[4];
+                cplx v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool in = e + u < e1;
+                    c[u] = in ? col[e + u] : -1;
+                    if (CV) v[u] = in ? ((const cplx *)valv)[e + u] : mk(0, 0);
+                    else v[u] = mk(in ? ((const double *)valv)[e + u] : 0.0, 0.0);
+                }
+                cplx x[4], xt[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    x[u] = c[u] >= 0 ? *rv.at((uint64_t)c[u]) : mk(0, 0);
+                    if (NRHS == 2) xt[u] = c[u] >= 0 ? *tv.at((uint64_t)c[u]) : mk(0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (CV) {
+                        acc = cfma(v[u], x[u], acc);
+                        if (NRHS == 2) acct = cfma(v[u], xt[u], acct);
+                    } else {
+                        acc.x = fma(v[u].x, x[u].x, acc.x);
+                        acc.y = fma(v[u].x, x[u].y, acc.y);
+                        if (NRHS == 2) { acct.x = fma(v[u].x, xt[u].x, acct.x); acct.y = fma(v[u].x, xt[u].y, acct.y); }
+                    }
+                }
+            }
+            a.q[i] = acc;
+            if (NRHS == 2) {
+                a.qt[i] = acct;
+                w = cfma_conj(t[i], acc, w);
+            } else {
+                w = cfma(r[i], acc, w);
+            }
+        }
+    }
+    spmv_exit(a, kp, agent, w, sc);
+}
+
 template <int LPR>
 static void csr_dispatch(const SpmvArgs &a, const KParams &kp, const int64_t *rp, const int32_t *col,
                          const void *val, bool cv, int grid, cudaStream_t s) {
@@ -419,9 +481,34 @@ static void csr_dispatch(const SpmvArgs &a, const KParams &kp, const int64_t *rp
     }
 }
 
+int csr_mode() {   // 0: lanes-per-row kernel, 1: row-per-thread kernel (default)
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("SHIFTK_CSR_ROW");
+        m = e ? atoi(e) : 1;
+    }
+    return m;
+}
+
+int csr_blocks(int64_t M) {
+    if (csr_mode() == 0) return stream_blocks(M);
+    int64_t b = (M + kThreads - 1) / kThreads;
+    return (int)(b > kMaxSpmvBlocks ? kMaxSpmvBlocks : (b < 1 ? 1 : b));
+}
+
 cudaError_t launch_csr(const SpmvArgs &a, const KParams &kp, const int64_t *rp, const int32_t *col,
                        const void *val, bool cv, double avg_nnz, cudaStream_t s) {
-    const int grid = stream_blocks(a.M) + (a.st ? 1 : 0);
+    const int grid = csr_blocks(a.M) + (a.st ? 1 : 0);
+    if (csr_mode() == 1) {
+        if (cv) {
+            if (a.bicg) csr_row_kernel<true, 2><<<grid, kThreads, 0, s>>>(a, kp, rp, col, val);
+            else csr_row_kernel<true, 1><<<grid, kThreads, 0, s>>>(a, kp, rp, col, val);
+        } else {
+            if (a.bicg) csr_row_kernel<false, 2><<<grid, kThreads, 0, s>>>(a, kp, rp, col, val);
+            else csr_row_kernel<false, 1><<<grid, kThreads, 0, s>>>(a, kp, rp, col, val);
+        }
+        return cudaGetLastError();
+    }
     if (avg_nnz <= 3.0) csr_dispatch<2>(a, kp, rp, col, val, cv, grid, s);
     else if (avg_nnz <= 6.0) csr_dispatch<4>(a, kp, rp, col, val, cv, grid, s);
     else if (avg_nnz <= 24.0) csr_dispatch<8>(a, kp, rp, col, val, cv, grid, s);
