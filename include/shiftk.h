@@ -76,7 +76,10 @@ enum sk_error {
 enum sk_mem { SK_MEM_HOST = 0, SK_MEM_DEVICE = 1 };
 
 enum sk_flags {
-    SK_FLAG_NO_SWITCH = 1   /* disable seed switching; diagnostics only           */
+    SK_FLAG_NO_SWITCH = 1,  /* disable seed switching; diagnostics only           */
+    SK_FLAG_LOG = 2         /* keep the coefficient log {alpha_n, beta_n, z_s, P r_n, switch
+                               factors, ||r_n||} for sk_recalc; itermax entries,
+                               itermax <= 2^24                                                 */
 };
 
 /* The operator H.  For SK_OP_HEISENBERG only L and J are read (M = 2^L, basis state s = L-bit
@@ -239,6 +242,14 @@ int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
 /* Diagnostics: %globaltimer stamps (ns) written by instrumented kernels (16 slots; see
    csrc/steps.cuh).  Requires the environment variable SHIFTK_DEBUG_TS at sk_init. */
 int sk_debug_timestamps(sk_ctx *ctx, int64_t *out16);
+
+/* Recalculation at new shifts (ShiftK "recalc"): the per-shift recurrences
+   EQ-SHIFTEDCG-PI/alpha/beta and EQ-SHIFTEDCG-y/u are replayed for z_new from the coefficient
+   log recorded so far — no operator application.  Each new shift is frozen when its residual
+   ||r_n|| / |pi_n| drops below tol, like the original shifts (R8), so recalc at the original
+   shifts reproduces sk_get_projection.  Requires SK_FLAG_LOG.  z_new: HOST [n_new];
+   y: HOST [n_new][n_left]; res: HOST [n_new] or NULL (residual at the last replayed step). */
+int sk_recalc(sk_ctx *ctx, int64_t n_new, const sk_cplx *z_new, sk_cplx *y, double *res);
 
 /* ---- multi-rank setup (see sk_dist) ---- */
 /* CUDA IPC handle (64 bytes) of this context's device arena, for the other ranks. */

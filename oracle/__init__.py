@@ -78,6 +78,9 @@ def lib():
                          ("or_retired_at", ctypes.c_void_p), ("or_y", ctypes.c_void_p)]:
             getattr(L, name).restype = rt
             getattr(L, name).argtypes = [ctypes.c_void_p]
+        L.or_recalc.argtypes = [ctypes.c_void_p, ctypes.c_int64, _c128p, ctypes.c_double, _c128p, ctypes.c_void_p]
+        L.or_log_length.restype = ctypes.c_int64
+        L.or_log_length.argtypes = [ctypes.c_void_p]
         L.or_x.restype = ctypes.c_void_p
         L.or_x.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.or_scalars.argtypes = [ctypes.c_void_p, _c128p]
@@ -153,6 +156,7 @@ class Oracle:
         self.nleft = 1 if left is None else self.left.shape[0]
         self.full_x = bool(full_x)
         self._keep = None if keep is None else np.ascontiguousarray(keep, dtype=np.uint8)
+        self.tol = tol
         self._h = lib().or_create_subset(self.method, self.M, self.nz, _ptr(self.z), _ptr(self.b),
                                          self.nleft, 0 if self.left is None else _ptr(self.left),
                                          int(self.full_x), float(tol), int(itermax), int(flags),
@@ -247,6 +251,19 @@ class Oracle:
         if not addr:
             raise ValueError(f"x of shift {k} not carried (keep mask)")
         return _view(addr, self.M, np.complex128)
+
+    def recalc(self, z_new, tol: Optional[float] = None):
+        """Projections at new shifts from the coefficient log, no operator use."""
+        z_new = np.ascontiguousarray(z_new, dtype=np.complex128)
+        y = np.zeros((z_new.shape[0], self.nleft), dtype=np.complex128)
+        res = np.zeros(z_new.shape[0], dtype=np.float64)
+        lib().or_recalc(self._h, z_new.shape[0], _ptr(z_new), float(self.tol if tol is None else tol),
+                        _ptr(y), res.ctypes.data)
+        return y, res
+
+    @property
+    def log_length(self) -> int:
+        return lib().or_log_length(self._h)
 
     def scalars(self) -> dict:
         out = np.zeros(6, dtype=np.complex128)

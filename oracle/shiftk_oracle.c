@@ -35,6 +35,9 @@
  *  10  nu = ||r_{n+1}||_2 ("2-norm"); res_k = nu / |pi_{n+1}^k| (EQ-COLLINEAR P:L300);
  *      retire k when res_k < tol (frozen thereafter, R8)
  *  11  CONVERGED when no shift is active; MAXITER when n+1 = itermax
+ *  log   (recalc) per iteration n: alpha_n, beta_{n-1}, c_n, z_s, g_n = P r_n,
+ *        nu = ||r_{n+1}|| and the switch factors 1/f, 1/f' (1 when no switch) — or_recalc replays
+ *        steps 6, 7 (projection), 10 for new shifts from this log with no operator application.
  *  12  seed switch ("always ... after an update"): s* = argmin_{k active} |pi_{n+1}^k|,
  *      lowest index on ties; if s* != s:  f = pi_{n+1}^{s*}, f' = pi_n^{s*};
  *      r_{n+1} /= f, r_n /= f' (shadow by conj);  active pi_{n+1} /= f, pi_n /= f';
@@ -71,6 +74,10 @@ typedef struct {
     unsigned char *keep;       /* full mode: which shifts carry x, p (all by default) */
     cplx alpha_prev, rho_prev;
     cplx alpha, beta, rho, w;  /* last iteration's seed scalars (for inspection) */
+    /* coefficient log for recalculation */
+    int64_t nlog, caplog;
+    cplx *lg_alpha, *lg_beta, *lg_c, *lg_zs, *lg_rf, *lg_rfp, *lg_g;   /* lg_g: [cap][nleft] */
+    double *lg_nu;
     int64_t n, nswitch, nspmv;
     int status;
 } or_state;
@@ -193,7 +200,25 @@ void or_destroy(or_state *st) {
     free(st->t); free(st->t_old); free(st->z); free(st->pi); free(st->pi_old); free(st->pi_new);
     free(st->active); free(st->res); free(st->retired_at); free(st->g); free(st->u); free(st->y);
     free(st->p); free(st->x); free(st->keep);
+    free(st->lg_alpha); free(st->lg_beta); free(st->lg_c); free(st->lg_zs); free(st->lg_rf);
+    free(st->lg_rfp); free(st->lg_g); free(st->lg_nu);
     free(st);
+}
+
+/* ------------------------------------------------------------------ coefficient log */
+
+static int log_reserve(or_state *st, int64_t n) {
+    if (n < st->caplog) return 1;
+    int64_t cap = st->caplog ? 2 * st->caplog : 64;
+    while (cap <= n) cap *= 2;
+#define GROW(f, T, w) do { T *p_ = (T *)realloc(st->f, (size_t)(cap * (w)) * sizeof(T)); \
+                           if (!p_) return 0; st->f = p_; } while (0)
+    GROW(lg_alpha, cplx, 1); GROW(lg_beta, cplx, 1); GROW(lg_c, cplx, 1); GROW(lg_zs, cplx, 1);
+    GROW(lg_rf, cplx, 1); GROW(lg_rfp, cplx, 1); GROW(lg_nu, double, 1);
+    GROW(lg_g, cplx, st->nleft);
+#undef GROW
+    st->caplog = cap;
+    return 1;
 }
 
 /* ------------------------------------------------------------------ one iteration */
@@ -223,6 +248,13 @@ int or_update(or_state *st, const cplx *q, const cplx *qt) {
 
     /* 6 + 7 */
     if (nl > 0) project(st, st->r, st->g);
+    const int logged = log_reserve(st, n);
+    if (logged) {
+        st->lg_alpha[n] = alpha; st->lg_beta[n] = beta; st->lg_c[n] = c; st->lg_zs[n] = st->zs;
+        for (int64_t l = 0; l < nl; ++l) st->lg_g[n * nl + l] = st->g[l];
+        st->lg_rf[n] = 1; st->lg_rfp[n] = 1; st->lg_nu[n] = 0;
+        st->nlog = n + 1;
+    }
     for (int64_t k = 0; k < nz; ++k) {
         if (!st->active[k]) continue;
         cplx sigma = st->z[k] - st->zs;
@@ -270,6 +302,7 @@ int or_update(or_state *st, const cplx *q, const cplx *qt) {
 
     /* 10 */
     double nu = sqrt(creal(dot_conj(st, st->r, st->r)));
+    if (logged) st->lg_nu[n] = nu;
     int64_t nact = 0;
     for (int64_t k = 0; k < nz; ++k) {
         if (!st->active[k]) continue;
@@ -304,11 +337,51 @@ int or_update(or_state *st, const cplx *q, const cplx *qt) {
             st->zs = st->z[best];
             st->s = best;
             st->nswitch++;
+            if (logged) { st->lg_rf[n] = 1.0 / f; st->lg_rfp[n] = 1.0 / fp; }
         }
     }
     if (st->n >= st->itermax) st->status = OR_MAXITER;
     return st->status;
 }
+
+/* ------------------------------------------------------------------ recalculation */
+
+/* Projections y[j][l] = a_l^dagger x^(z_j) for new shifts from the coefficient log (P:L640-651:
+   "the recurrence relations for the shifted equation ... can be solved without any expensive
+   matrix-vector multiplications"): for each new shift, steps 6, 7 (projection) and 10 of
+   or_update replayed with the logged alpha_n, beta_{n-1}, c_n, z_s, g_n, nu and switch
+   factors; the shift is frozen (R8) when its residual drops below tol.  res[j]: last residual. */
+void or_recalc(const or_state *st, int64_t nnew, const cplx *znew, double tol, cplx *y, double *res) {
+    const int64_t nl = st->nleft;
+    cplx *u = (cplx *)xcalloc(nl, sizeof(cplx));
+    for (int64_t j = 0; j < nnew; ++j) {
+        cplx pi = 1, pio = 1;
+        double rj = sqrt(creal(dot_conj(st, st->b, st->b)));
+        for (int64_t l = 0; l < nl; ++l) { u[l] = 0; y[j * nl + l] = 0; }
+        for (int64_t n = 0; n < st->nlog; ++n) {
+            const cplx alpha = st->lg_alpha[n], beta = st->lg_beta[n], c = st->lg_c[n];
+            const cplx sigma = znew[j] - st->lg_zs[n];
+            const cplx pin = (1.0 + c + alpha * sigma) * pi - c * pio;
+            const cplx ak = (pi / pin) * alpha;
+            const cplx rat = pio / pi;
+            const cplx bk = (n == 0) ? 0 : rat * rat * beta;
+            for (int64_t l = 0; l < nl; ++l) {
+                u[l] = st->lg_g[n * nl + l] / pi + bk * u[l];
+                y[j * nl + l] += ak * u[l];
+            }
+            pio = pi;
+            pi = pin;
+            rj = st->lg_nu[n] / cabs(pi);
+            if (rj < tol) break;
+            pi *= st->lg_rf[n];
+            pio *= st->lg_rfp[n];
+        }
+        if (res) res[j] = rj;
+    }
+    free(u);
+}
+
+int64_t or_log_length(const or_state *st) { return st->nlog; }
 
 /* ------------------------------------------------------------------ operators */
 

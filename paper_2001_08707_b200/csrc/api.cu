@@ -113,6 +113,7 @@ struct sk_ctx {
     bool connected = true;          // false until sk_connect / sk_group_connect
     void *arena = nullptr;
     size_t arena_bytes = 0;
+    double b_norm = 0;              // ||b|| (global), recorded at initialisation
     std::vector<void *> peer_bases; // opened IPC mappings of the other ranks' arenas
 };
 
@@ -287,6 +288,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         return fail(SK_EINVAL, "n_left/left inconsistent");
     if (p->n_left > 32) return fail(SK_EUNSUPPORTED, "n_left > 32");
     if (p->n_shift > (1 << 20)) return fail(SK_EUNSUPPORTED, "n_shift > 2^20");
+    if ((p->flags & SK_FLAG_LOG) && p->itermax > (int64_t(1) << 24))
+        return fail(SK_EINVAL, "SK_FLAG_LOG needs itermax <= 2^24 (one log entry per iteration)");
     const int64_t M = H->M_local > 0 ? H->M_local : H->M;
     if (world > 1) {   // rows [rank * M_local, (rank + 1) * M_local), M_local a power of two
         if (M * world != H->M || (M & (M - 1)) != 0 || H->row_begin != (int64_t)rank * M)
@@ -399,6 +402,12 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&kp.y, sizeof(cplx) * c->nz * c->nl);
         add(&kp.g, sizeof(cplx) * c->nl);
         if (getenv("SHIFTK_DEBUG_TS")) add(&kp.dbg_ts, sizeof(int64_t) * 16);
+        if (p->flags & SK_FLAG_LOG) {
+            kp.lg_cap = p->itermax;
+            add(&kp.lg, sizeof(cplx) * 6 * (size_t)p->itermax);
+            add(&kp.lg_nu, sizeof(double) * (size_t)p->itermax);
+            add(&kp.lg_g, sizeof(cplx) * (size_t)p->itermax * c->nl);
+        }
         if (world > 1) {
             add(&kp.wloc, sizeof(cplx));
             add(&kp.wsum, sizeof(cplx));
@@ -476,6 +485,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     if (sk::launch_scalar(kp, sk::PH_INIT, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init scalar"));
     if ((rc = read_state(c)) != SK_OK) return bail(rc);
     if (!(c->st_host->nu > 0)) return bail(fail(SK_EINVAL, "||b|| must be > 0"));
+    c->b_norm = c->st_host->nu;
     *out = c;
     return SK_OK;
 }
@@ -500,7 +510,39 @@ static int finish_init(sk_ctx *c) {
     int rc;
     if ((rc = read_state(c)) != SK_OK) return rc;
     if (!(c->st_host->nu > 0)) return fail(SK_EINVAL, "||b|| must be > 0");
+    c->b_norm = c->st_host->nu;
     c->connected = true;
+    return SK_OK;
+}
+
+int sk_recalc(sk_ctx *c, int64_t n_new, const sk_cplx *z_new, sk_cplx *y, double *res) {
+    if (!c || !z_new || !y) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (!c->kp.lg) return fail(SK_ESTATE, "context created without SK_FLAG_LOG");
+    if (n_new < 1 || n_new > (1 << 24)) return fail(SK_EINVAL, "n_new");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    const int64_t nlog = c->st_host->n < c->kp.lg_cap ? c->st_host->n : c->kp.lg_cap;
+    // ||b|| = ||r_0||: the residual of a shift before any iteration
+    double nu0 = 0;
+    {
+        const size_t nv = (size_t)n_new * c->nl;
+        void *tmp = nullptr;
+        const size_t bytes = sizeof(cplx) * (n_new + 2 * nv) + sizeof(double) * n_new;
+        CK(cudaMallocAsync(&tmp, bytes, c->stream));
+        cplx *zd = (cplx *)tmp, *yd = zd + n_new, *ud = yd + nv;
+        double *rd = (double *)(ud + nv);
+        CK(cudaMemcpyAsync(zd, z_new, sizeof(cplx) * n_new, cudaMemcpyHostToDevice, c->stream));
+        nu0 = c->b_norm;
+        CK(sk::launch_recalc(c->kp, nlog, zd, (int)n_new, c->tol, nu0, yd, ud, rd, c->stream));
+        CK(cudaMemcpyAsync(y, yd, sizeof(cplx) * nv, cudaMemcpyDeviceToHost, c->stream));
+        std::vector<double> rh(n_new);
+        CK(cudaMemcpyAsync(rh.data(), rd, sizeof(double) * n_new, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaFreeAsync(tmp, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (res) memcpy(res, rh.data(), sizeof(double) * n_new);
+    }
     return SK_OK;
 }
 

@@ -155,6 +155,11 @@ struct KParams {
     cplx *wloc, *wsum;           // [1] this rank's / all-reduced SpMV dot  (world > 1)
     cplx *uloc, *usum;           // [2 + nl] this rank's / all-reduced update dots (world > 1)
     uint32_t *ticket_u;          // [1] last-CTA detection in the update kernel (world > 1)
+    // ---- coefficient log for recalculation (SK_FLAG_LOG) ----
+    cplx *lg;                    // [lg_cap][6]: alpha_n, beta_{n-1}, c_n, z_s(n), 1/f, 1/f'
+    double *lg_nu;               // [lg_cap]: ||r_{n+1}|| (before the switch of iteration n)
+    cplx *lg_g;                  // [lg_cap][nl]: P r_n
+    int64_t lg_cap;
 };
 
 // Per shift-agent result: argmin over its slice of |pi_{n+1}|^2 (lowest index on ties).

@@ -46,6 +46,10 @@ cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cuda
 enum : int { PH_INIT = 1, PH_FINISH = 2 };
 cudaError_t launch_scalar(const KParams &kp, int phase, cudaStream_t s);
 
+// Recalculation at new shifts from the coefficient log (y, u: device [nnew][nl], res [nnew]).
+cudaError_t launch_recalc(const KParams &kp, int64_t nlog, const cplx *znew, int nnew, double tol,
+                          double nu0, cplx *y, cplx *u, double *res, cudaStream_t s);
+
 // ---- multi-rank (world > 1) -----------------------------------------------------------------
 constexpr int kMaxWorld = 64;
 struct LoopbackPtrs {

@@ -17,7 +17,10 @@ __global__ void __launch_bounds__(kThreads) scalar_kernel(KParams kp, int phase)
         else reduce_columns(kp.part_u, kp.nblk_upd, 2 + kp.nl, 2 + kp.nl, sc);   // (barriers publish)
         const double nu = sqrt(sc.col[1].x);
         for (int k = threadIdx.x; k < kp.nz; k += blockDim.x) kp.res[k] = nu;
-        if (threadIdx.x < kp.nl) kp.g[threadIdx.x] = sc.col[2 + threadIdx.x];
+        if (threadIdx.x < kp.nl) {
+            kp.g[threadIdx.x] = sc.col[2 + threadIdx.x];
+            if (kp.lg_cap > 0) kp.lg_g[threadIdx.x] = sc.col[2 + threadIdx.x];   // P r_0
+        }
         if (threadIdx.x == 0) {
             sc.S.rho_cur = sc.col[0];
             sc.S.nu = nu;
@@ -39,13 +42,53 @@ cudaError_t launch_scalar(const KParams &kp, int phase, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- recalculation
+// Projections at new shifts from the coefficient log: the per-shift recurrences
+// (a4, a6) and the residual test (a8) replayed with the logged seed scalars, seed shifts,
+// P r_n and switch factors — one thread per new shift, no operator application.
+__global__ void recalc_kernel(KParams kp, int64_t nlog, const cplx *__restrict__ znew, int nnew,
+                              double tol, double nu0, cplx *__restrict__ y, cplx *__restrict__ u,
+                              double *__restrict__ res) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nnew) return;
+    const int nl = kp.nl;
+    const cplx z = znew[j];
+    cplx pi = mk(1, 0), pio = mk(1, 0);
+    double rj = nu0;
+    for (int l = 0; l < nl; ++l) { u[(int64_t)j * nl + l] = mk(0, 0); y[(int64_t)j * nl + l] = mk(0, 0); }
+    for (int64_t n = 0; n < nlog; ++n) {
+        const cplx *e = kp.lg + 6 * n;
+        const ShiftCoef sc = shift_coef(pi, pio, z, e[3], e[0], e[1], e[2], n);
+        for (int l = 0; l < nl; ++l) {
+            const int64_t o = (int64_t)j * nl + l;
+            const cplx uu = cadd(cmul(kp.lg_g[n * nl + l], sc.ipik), cmul(sc.bk, u[o]));
+            u[o] = uu;
+            y[o] = cfma(sc.ak, uu, y[o]);
+        }
+        pio = pi;
+        pi = sc.pin;
+        double r2;
+        if (retire_test(kp.lg_nu[n], pi, tol, r2)) { rj = r2; break; }
+        rj = r2;
+        pi = cmul(pi, e[4]);
+        pio = cmul(pio, e[5]);
+    }
+    res[j] = rj;
+}
+
+cudaError_t launch_recalc(const KParams &kp, int64_t nlog, const cplx *znew, int nnew, double tol,
+                          double nu0, cplx *y, cplx *u, double *res, cudaStream_t s) {
+    recalc_kernel<<<(nnew + 127) / 128, 128, 0, s>>>(kp, nlog, znew, nnew, tol, nu0, y, u, res);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- multi-rank (world > 1)
 // Seed step on the all-reduced w (the single-GPU path runs it in the SpMV's last CTA).
 __global__ void __launch_bounds__(kThreads) seed_kernel(KParams kp) {
     __shared__ StepScratch sc;
     state_load_nosync(sc.S, kp.st);
     __syncthreads();
-    if (threadIdx.x == 0 && sc.S.status == ST_ITERATING) seed_step(&sc.S, __ldcg(kp.wsum), kp.bicg);
+    if (threadIdx.x == 0 && sc.S.status == ST_ITERATING) seed_step(&sc.S, __ldcg(kp.wsum), kp.bicg, kp);
     __syncthreads();
     if (sc.S.status == ST_BREAKDOWN && sc.S.lz_pending) retire_pass(kp, sc);
     state_store(kp.st, sc.S);

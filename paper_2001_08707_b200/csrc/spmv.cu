@@ -100,7 +100,7 @@ __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParams &kp, 
     state_load_nosync(sc.S, kp.st);
     reduce_columns(a.part_w, gridDim.x - 1, 1, 1, sc);   // (its barriers publish sc.S)
     if (threadIdx.x == 0) {
-        if (sc.S.status == ST_ITERATING) seed_step(&sc.S, sc.col[0], a.bicg);
+        if (sc.S.status == ST_ITERATING) seed_step(&sc.S, sc.col[0], a.bicg, kp);
         *kp.ticket = 0u;
     }
     __syncthreads();

@@ -260,6 +260,11 @@ static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eage
             S->seed = bst;
             S->nswitch += 1;
         }
+        if (m < kp.lg_cap) {   // coefficient log (recalc): nu before the switch, switch factors
+            kp.lg_nu[m] = nu;
+            kp.lg[6 * m + 4] = rf;
+            kp.lg[6 * m + 5] = sw ? xrecip(fp) : mk(1, 0);
+        }
         S->rho_cur = cmul(sc.col[0], cmul(rf, rf));                       // rho_{m+1} / f^2
         S->nu = nu * sqrt(cabs2(rf));
         S->lz_pending = 1;
@@ -272,14 +277,18 @@ static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eage
         sc.bi[0] = all_retire || S->status != ST_ITERATING;
     }
     __syncthreads();
-    if (threadIdx.x < nl) kp.g[threadIdx.x] = cmul(sc.col[2 + threadIdx.x], sc.bc[0]);
+    if (threadIdx.x < nl) {
+        const cplx gl = cmul(sc.col[2 + threadIdx.x], sc.bc[0]);
+        kp.g[threadIdx.x] = gl;
+        if (m + 1 < kp.lg_cap) kp.lg_g[(m + 1) * nl + threadIdx.x] = gl;   // P r_{m+1}
+    }
     if (eager || sc.bi[0]) retire_pass(kp, sc);
     state_store(kp.st, sc.S);
 }
 
 // ------------------------------------------------------------------------------- seed_step
 // One thread, on a shared copy of the state.  w_raw = <r~|r, q> of the stored vectors.
-static __device__ void seed_step(DevState *S, cplx wraw, int bicg) {
+static __device__ void seed_step(DevState *S, cplx wraw, int bicg, const KParams &kp) {
     const cplx sr = S->sr_cur;
     const cplx w = cmul(cmul(sr, sr), wraw);   // true-scale w_n (shadow scale = conj(sr))
     const cplx rho = S->rho_cur;
@@ -302,6 +311,14 @@ static __device__ void seed_step(DevState *S, cplx wraw, int bicg) {
     S->beta = beta;
     S->c = c;
     S->sr_it = sr;
+    if (n < kp.lg_cap) {   // coefficient log (recalc)
+        kp.lg[6 * n] = alpha;
+        kp.lg[6 * n + 1] = beta;
+        kp.lg[6 * n + 2] = c;
+        kp.lg[6 * n + 3] = S->zs;
+        kp.lg[6 * n + 4] = mk(1, 0);
+        kp.lg[6 * n + 5] = mk(1, 0);
+    }
     const cplx c1 = cadd(mk(1.0, 0.0), c);
     S->a_cur = cmul(csub(c1, cmul(alpha, S->zs)), sr);   // EQ-CG-RN-3REC with A r = z_s r - q
     S->a_q = cmul(alpha, sr);

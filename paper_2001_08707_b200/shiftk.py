@@ -23,6 +23,7 @@ ITERATING, CONVERGED, MAXITER, BREAKDOWN = 0, 1, 2, 3
 STATUS_NAMES = {0: "iterating", 1: "converged", 2: "maxiter", 3: "breakdown"}
 MEM_HOST, MEM_DEVICE = 0, 1
 FLAG_NO_SWITCH = 1
+FLAG_LOG = 2
 ERRORS = {0: "SK_OK", -1: "SK_EINVAL", -2: "SK_ENOMEM", -3: "SK_ECUDA", -4: "SK_ENCCL",
           -5: "SK_ESTATE", -6: "SK_EUNSUPPORTED"}
 EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_run", "sk_enqueue",
@@ -30,7 +31,7 @@ EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_ru
            "sk_get_coefficients", "sk_finalize", "sk_apply_operator", "sk_last_error", "sk_version",
            "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
            "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
-           "sk_group_update", "sk_group_run", "sk_group_destroy"]
+           "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc"]
 
 
 class ShiftkError(RuntimeError):
@@ -114,6 +115,7 @@ def load(path: str = LIB_PATH):
         "sk_group_update": [VP, P(I32)],
         "sk_group_run": [VP, I64, P(I32)],
         "sk_group_destroy": [P(VP)],
+        "sk_recalc": [VP, I64, VP, VP, VP],
         "sk_get_profile": [VP, P(sk_profile), I32],
     }
     for name, args in sig.items():
@@ -322,6 +324,15 @@ class Solver:
         out = np.empty(self.M, dtype=np.complex128)
         _check(load().sk_copy_solution(self._h, k, out.ctypes.data, MEM_HOST), "sk_copy_solution")
         return out
+
+    def recalc(self, z_new):
+        """Projections (and residuals) at new shifts from the coefficient log (SK_FLAG_LOG)."""
+        z_new = np.ascontiguousarray(z_new, dtype=np.complex128)
+        y = np.empty((z_new.shape[0], self.nl), dtype=np.complex128)
+        res = np.empty(z_new.shape[0], dtype=np.float64)
+        _check(load().sk_recalc(self._h, z_new.shape[0], z_new.ctypes.data, y.ctypes.data, res.ctypes.data),
+               "sk_recalc")
+        return y, res
 
     def shift_state(self):
         pi = np.empty(self.nz, dtype=np.complex128)

@@ -436,3 +436,25 @@ def test_edge_invalid_arguments():
         oracle.Oracle("cocg", b, np.array([0.1j]), tol=0.0)
     with pytest.raises(ValueError):
         oracle.Oracle("cocg", b, np.array([0.1j]), itermax=0)
+
+
+def test_recalc_identity_and_new_shifts_vs_dense():
+    """Recalculation from the coefficient log: replaying the logged recurrences at
+    the original shifts reproduces the run's projections; at new shifts between
+    them it matches a dense solve within the replayed residual's bound."""
+    L = 10
+    p = synth.make_problem("c2", L=L, nz=32)
+    o = oracle.solve(p)
+    assert o.status == oracle.CONVERGED and o.log_length == o.iterations
+    y, res = o.recalc(p.z)
+    assert np.max(np.abs(y - o.projections())) <= 1e-12 * np.max(np.abs(o.projections()))
+    assert np.all(res < p.tol)
+    H, _ = dense_heisenberg(L)
+    lam, U = np.linalg.eigh(H)
+    Ub = U.T @ p.b
+    z_new = synth.spectrum_shifts(31, -10.0 + 14.0 / 64, 4.0 + 14.0 / 64, 0.05)   # midpoints
+    y2, res2 = o.recalc(z_new)
+    for k, z in enumerate(z_new):
+        exact = np.vdot(p.b, U @ (Ub / (z - lam)))
+        assert abs(y2[k, 0] - exact) <= (res2[k] + 1e-12) / 0.05
+    assert o.spmv_count == o.iterations     # recalc used no operator application
