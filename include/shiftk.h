@@ -33,6 +33,7 @@
 #ifndef SHIFTK_H
 #define SHIFTK_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -250,6 +251,15 @@ int sk_debug_timestamps(sk_ctx *ctx, int64_t *out16);
    shifts reproduces sk_get_projection.  Requires SK_FLAG_LOG.  z_new: HOST [n_new];
    y: HOST [n_new][n_left]; res: HOST [n_new] or NULL (residual at the last replayed step). */
 int sk_recalc(sk_ctx *ctx, int64_t n_new, const sk_cplx *z_new, sk_cplx *y, double *res);
+
+/* Checkpoint / restart ("initial values of the coefficients and the vector", P:L575
+   calctype = restart; SURVEY f-4).  sk_checkpoint copies the complete solver state (seed
+   residuals with their lazy scales, seed and per-shift scalars, projections, full-mode x/p,
+   coefficient log) to host memory: call with buf = NULL to get the size in *bytes.
+   sk_restore loads it into a context created by sk_init with the SAME operator, parameters and
+   placement; the continued run is bit-identical to an uninterrupted one. */
+int sk_checkpoint(sk_ctx *ctx, void *buf, size_t *bytes);
+int sk_restore(sk_ctx *ctx, const void *buf, size_t bytes);
 
 /* ---- multi-rank setup (see sk_dist) ---- */
 /* CUDA IPC handle (64 bytes) of this context's device arena, for the other ranks. */

@@ -546,6 +546,65 @@ int sk_recalc(sk_ctx *c, int64_t n_new, const sk_cplx *z_new, sk_cplx *y, double
     return SK_OK;
 }
 
+// The arena holds every piece of solver state (borrowed inputs — CSR, device left vectors —
+// live outside it), so a checkpoint is the arena bytes plus a small header; pointers inside it
+// are not stored (buffers are addressed through KParams, rebuilt identically by sk_init).
+struct CkptHeader {
+    uint64_t magic, arena_bytes;
+    int64_t M, nz, nl, world, rank;
+    int32_t method, full;
+};
+static const uint64_t kCkptMagic = 0x314b5054504b4b53ull;   // "SKKPTPK1"
+
+int sk_checkpoint(sk_ctx *c, void *buf, size_t *bytes) {
+    if (!c || !bytes) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    const size_t need = sizeof(CkptHeader) + c->arena_bytes;
+    if (!buf) { *bytes = need; return SK_OK; }
+    if (*bytes < need) return fail(SK_EINVAL, "checkpoint buffer too small");
+    CK(cudaSetDevice(c->device));
+    int rc;
+    if ((rc = enqueue_finish(c)) != SK_OK) return rc;
+    CkptHeader h{kCkptMagic, c->arena_bytes, c->M, c->nz, c->nl, c->world, c->rank, c->method, c->full};
+    memcpy(buf, &h, sizeof(h));
+    CK(cudaMemcpyAsync((char *)buf + sizeof(h), c->arena, c->arena_bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *bytes = need;
+    return SK_OK;
+}
+
+int sk_restore(sk_ctx *c, const void *buf, size_t bytes) {
+    if (!c || !buf) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    CkptHeader h;
+    if (bytes < sizeof(h)) return fail(SK_EINVAL, "checkpoint too small");
+    memcpy(&h, buf, sizeof(h));
+    if (h.magic != kCkptMagic || h.arena_bytes != c->arena_bytes || h.M != c->M || h.nz != c->nz ||
+        h.nl != c->nl || h.world != c->world || h.rank != c->rank || h.method != c->method || h.full != c->full ||
+        bytes < sizeof(h) + h.arena_bytes)
+        return fail(SK_EINVAL, "checkpoint does not match this context (operator/parameters/placement)");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    // the shard tables hold this process's peer mappings: keep them across the restore
+    std::vector<char> keep_r, keep_t;
+    const size_t tab = sizeof(cplx *) * 3 * c->world;
+    if (c->world > 1) {
+        keep_r.resize(tab);
+        keep_t.resize(tab);
+        CK(cudaMemcpy(keep_r.data(), c->kp.shard_r, tab, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(keep_t.data(), c->kp.shard_t, tab, cudaMemcpyDeviceToHost));
+    }
+    CK(cudaMemcpyAsync(c->arena, (const char *)buf + sizeof(h), c->arena_bytes, cudaMemcpyHostToDevice, c->stream));
+    if (c->world > 1) {
+        CK(cudaMemcpyAsync((void *)c->kp.shard_r, keep_r.data(), tab, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync((void *)c->kp.shard_t, keep_t.data(), tab, cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->pending_host = false;   // the checkpoint was taken after a finish
+    int rc;
+    if ((rc = read_state(c)) != SK_OK) return rc;
+    c->host_started = c->st_host->n_started;
+    return SK_OK;
+}
+
 int sk_ipc_handle(sk_ctx *c, void *out64) {
     if (!c || !out64) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
     cudaIpcMemHandle_t h;

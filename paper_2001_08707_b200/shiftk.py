@@ -31,7 +31,8 @@ EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_ru
            "sk_get_coefficients", "sk_finalize", "sk_apply_operator", "sk_last_error", "sk_version",
            "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
            "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
-           "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc"]
+           "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc", "sk_checkpoint",
+           "sk_restore"]
 
 
 class ShiftkError(RuntimeError):
@@ -116,6 +117,8 @@ def load(path: str = LIB_PATH):
         "sk_group_run": [VP, I64, P(I32)],
         "sk_group_destroy": [P(VP)],
         "sk_recalc": [VP, I64, VP, VP, VP],
+        "sk_checkpoint": [VP, VP, P(ctypes.c_size_t)],
+        "sk_restore": [VP, VP, ctypes.c_size_t],
         "sk_get_profile": [VP, P(sk_profile), I32],
     }
     for name, args in sig.items():
@@ -333,6 +336,17 @@ class Solver:
         _check(load().sk_recalc(self._h, z_new.shape[0], z_new.ctypes.data, y.ctypes.data, res.ctypes.data),
                "sk_recalc")
         return y, res
+
+    def checkpoint(self) -> bytes:
+        """Complete solver state (restart: P:L520)."""
+        n = ctypes.c_size_t(0)
+        _check(load().sk_checkpoint(self._h, None, ctypes.byref(n)), "sk_checkpoint")
+        buf = ctypes.create_string_buffer(n.value)
+        _check(load().sk_checkpoint(self._h, buf, ctypes.byref(n)), "sk_checkpoint")
+        return buf.raw[:n.value]
+
+    def restore(self, blob: bytes):
+        _check(load().sk_restore(self._h, blob, len(blob)), "sk_restore")
 
     def shift_state(self):
         pi = np.empty(self.nz, dtype=np.complex128)

@@ -313,3 +313,27 @@ def test_recalc_parity(name, kw):
     # then report a residual above tol, of the same size)
     assert np.all((rg < p.tol) == (ro < p.tol)) or np.all(np.abs(np.log10(rg / ro)) < 1)
     assert g.coefficients()["spmv_count"] == g.coefficients()["iterations"] * (2 if p.method == "bicg" else 1)
+
+
+@pytest.mark.parametrize("name,kw", [("c1", dict(L=10, nz=8)), ("c4", dict(W=12, nz=8, n_left=4))])
+def test_checkpoint_restart_bitwise(name, kw):
+    """Restart (SURVEY f-4): k iterations, checkpoint, restore into a fresh
+    context, continue — bit-identical to the uninterrupted run (full x included)."""
+    p = synth.make_problem(name, **kw)
+    dp = to_device(p)
+    a = make_solver(dp, flags=shiftk.FLAG_LOG, itermax=3000)
+    a.run(37)
+    blob = a.checkpoint()
+    b = make_solver(dp, flags=shiftk.FLAG_LOG, itermax=3000)
+    b.restore(blob)
+    a.run(3000)
+    b.run(3000)
+    assert a.coefficients() == b.coefficients()
+    assert np.array_equal(a.projections(), b.projections())
+    assert np.array_equal(a.residuals(), b.residuals())
+    if p.full_x:
+        assert np.array_equal(a.solution(3), b.solution(3))
+    assert np.array_equal(a.recalc(p.z)[0], b.recalc(p.z)[0])
+    c = make_solver(to_device(synth.make_problem(name, **dict(kw, nz=kw["nz"] + 1))))
+    with pytest.raises(shiftk.ShiftkError):
+        c.restore(blob)
