@@ -21,10 +21,13 @@ def _nccl_dir():
 
 
 NCCL_DIR = _nccl_dir()
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC,-O2", "-shared", "-I" + os.path.join(ROOT, "include"),
-         "-I" + os.path.join(NCCL_DIR, "include"), "--expt-relaxed-constexpr",
-         '-DSHIFTK_NCCL_DEFAULT="' + os.path.join(NCCL_DIR, "lib", "libnccl.so.2") + '"', "-ldl"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+                 "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(NCCL_DIR, "include"),
+                 "--expt-relaxed-constexpr",
+                 '-DSHIFTK_NCCL_DEFAULT="' + os.path.join(NCCL_DIR, "lib", "libnccl.so.2") + '"']
+LDFLAGS = ARCH + ["-shared", "-ldl"]
+OBJDIR = os.path.join(HERE, "_obj")
 
 
 def sources():
@@ -42,10 +45,22 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB] + sources()
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    # one nvcc per translation unit, in parallel (the tiled SpMV instantiations dominate)
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs, procs = [], []
+    for src in sources():
+        obj = os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC] + CFLAGS + ["-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd), src))
+        objs.append(obj)
+    bad = [src for pr, src in procs if pr.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, "nvcc " + " ".join(bad))
+    tmp = LIB + ".tmp"
+    subprocess.check_call([NVCC] + LDFLAGS + ["-o", tmp] + objs)
+    os.replace(tmp, LIB)
     return LIB
 
 

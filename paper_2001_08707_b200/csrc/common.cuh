@@ -36,6 +36,10 @@ __device__ __forceinline__ void dbg_stamp(int64_t *ts, int i) {
     }
 }
 
+// griddepcontrol.wait: returns when the programmatic predecessor grid has completed (a no-op for
+// kernels launched without the PDL attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ cplx warp_sum(cplx v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

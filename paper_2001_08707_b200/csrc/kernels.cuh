@@ -1,8 +1,32 @@
 // kernels.cuh — launch wrappers of the hot-path kernels (spmv.cu, update.cu, scalar.cu).
 #pragma once
+#include <utility>
+
 #include "common.cuh"
 
 namespace sk {
+
+// Programmatic dependent launch (PDL): the SpMV and update kernels of the iteration loop are
+// launched with programmatic stream serialization, so a kernel's CTAs are dispatched while its
+// predecessor drains; each such kernel's first instruction is griddepcontrol.wait, which
+// returns once the predecessor has completed and its writes are visible — the data order is
+// unchanged, only the launch latency is hidden.  SHIFTK_PDL=0 disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                     bool pdl, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr int kThreads = 256;          // streaming kernels
 constexpr int kScalarThreads = 1024;   // the single-CTA init / finish kernel
@@ -29,6 +53,11 @@ struct SpmvArgs {
     int bicg;
 };
 cudaError_t launch_heisenberg(const SpmvArgs &a, const KParams &kp, int L, double J, cudaStream_t s);
+// tiled Heisenberg SpMV by chain length: a 11..16, b 17..22, c 23..28, d 29..34 (spmv_tiled_*.cu)
+cudaError_t launch_tiled_a(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);
+cudaError_t launch_tiled_b(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);
+cudaError_t launch_tiled_c(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);
+cudaError_t launch_tiled_d(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);
 cudaError_t launch_csr(const SpmvArgs &a, const KParams &kp, const int64_t *row_ptr, const int32_t *col,
                        const void *val, bool cplx_val, double avg_nnz, cudaStream_t s);
 // Reverse communication: a.q holds the caller's q = H r.

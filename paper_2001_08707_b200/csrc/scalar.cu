@@ -32,9 +32,17 @@ __global__ void __launch_bounds__(kThreads) scalar_kernel(KParams kp, int phase)
         state_store(kp.st, sc.S);
         return;
     }
-    // FINISH: only when an iteration is pending (the state is read through L2)
+    // FINISH: of a pending iteration; or, after a breakdown in the seed step, the retirement
+    // test that the finish of the previous iteration left pending (the state is read via L2)
     const int pending = __ldcg(&kp.st->pending);
-    if (pending) finish_step(kp, sc, /*eager=*/true);
+    if (pending) {
+        finish_step(kp, sc, /*eager=*/true);
+    } else if (__ldcg(&kp.st->status) == ST_BREAKDOWN && __ldcg(&kp.st->lz_pending)) {
+        state_load_nosync(sc.S, kp.st);
+        __syncthreads();
+        retire_pass(kp, sc);
+        state_store(kp.st, sc.S);
+    }
 }
 
 cudaError_t launch_scalar(const KParams &kp, int phase, cudaStream_t s) {
@@ -89,8 +97,6 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(KParams kp) {
     state_load_nosync(sc.S, kp.st);
     __syncthreads();
     if (threadIdx.x == 0 && sc.S.status == ST_ITERATING) seed_step(&sc.S, __ldcg(kp.wsum), kp.bicg, kp);
-    __syncthreads();
-    if (sc.S.status == ST_BREAKDOWN && sc.S.lz_pending) retire_pass(kp, sc);
     state_store(kp.st, sc.S);
 }
 

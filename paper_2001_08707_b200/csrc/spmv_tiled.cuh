@@ -1,0 +1,183 @@
+// spmv_tiled.cuh — the tiled Heisenberg SpMV kernel (one instantiation per chain length L;
+// the instantiations are spread over spmv_tiled_*.cu so they compile in parallel).
+#pragma once
+#include "spmv_common.cuh"
+
+namespace sk {
+
+// Tiled kernel (bond-major within a tile of 2^T states).  Each thread owns PER = 2^T/256
+// states (ls = tid + 256 k) with q in registers.
+//   round 1: own tile (-> shared memory + diagonal), bond (T-1,T) and the periodic bond (L-1,0),
+//            3*PER independent loads in flight per thread;
+//   rounds 2..: the ACTIVE tile-level bonds i >= T (a bond flips two tile-index bits, so the
+//            whole tile takes part or none: the active set is uniform per CTA), three partner
+//            tiles per round, each a coalesced stream;
+//   then the T-1 bonds inside the tile from shared memory.
+template <int L, int T, int NRHS, bool MULTI>
+__global__ void __launch_bounds__(kThreads, NRHS == 1 ? 4 : 2)
+heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
+    extern __shared__ cplx tile[];   // [NRHS][2^T]
+    __shared__ StepScratch sc;
+    using U = typename std::conditional<(L <= 31), uint32_t, uint64_t>::type;
+    bool agent;
+    int buf;
+    if (!spmv_enter(a, agent, buf, sc, kp)) return;
+    constexpr int TS = 1 << T;
+    constexpr int PER = TS / kThreads;
+    constexpr int NB = 3;
+    static_assert(PER * kThreads == TS, "tile must be a multiple of the CTA size");
+    const cplx *__restrict__ r = pick3(a.r, buf);
+    const cplx *__restrict__ t = pick3(a.t, buf);
+    // global view of r (and r~): with world > 1 partner tiles on other ranks are read in place
+    // through peer memory; every partner tile below is resolved once per tile (its shard is
+    // uniform over the tile).
+    const RViewT<MULTI> rv = rview<MULTI>(r, kp.shard_r, buf, kp), tv = rview<MULTI>(t, kp.shard_t, buf, kp);
+    const double qJ = 0.25 * J, hJ = 0.5 * J;
+    const int64_t ntiles = a.M >> T;
+    const int tid = threadIdx.x;
+    const int off = a.st ? 1 : 0;
+    cplx w = mk(0.0, 0.0);
+    for (int64_t ti = (int64_t)blockIdx.x - off; !agent && ti < ntiles; ti += gridDim.x - off) {
+        const int64_t lbase = ti << T;                  // local row of the tile
+        const U base = (U)((MULTI ? rv.row0 : 0) + lbase);   // global basis state of the tile
+        __syncthreads();   // previous tile's shared-memory reads are done
+        cplx q[PER], qt[NRHS == 2 ? PER : 1];
+        {
+            cplx v0[PER], v1[PER], v2[PER], t0[NRHS == 2 ? PER : 1], t1[NRHS == 2 ? PER : 1],
+                t2[NRHS == 2 ? PER : 1];
+            const U tb = (base >> T) & (U)1, hb = (base >> (L - 1)) & (U)1;
+            // partner tiles: bond (T-1, T) flips bit T (and bit T-1 inside the tile); the
+            // periodic bond (L-1, 0) flips bit L-1 (and bit 0 inside the tile)
+            const cplx *p1 = rv.at(base ^ ((U)1 << T)), *p2 = rv.at(base ^ ((U)1 << (L - 1)));
+            const cplx *p1t = nullptr, *p2t = nullptr;
+            if (NRHS == 2) { p1t = tv.at(base ^ ((U)1 << T)); p2t = tv.at(base ^ ((U)1 << (L - 1))); }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int ls = tid + k * kThreads;
+                v0[k] = r[lbase + ls];
+                if (NRHS == 2) t0[k] = t[lbase + ls];
+                const bool on1 = ((U)((ls >> (T - 1)) & 1) ^ tb) != 0;    // bond (T-1, T)
+                const int l1 = ls ^ (1 << (T - 1));
+                v1[k] = on1 ? p1[l1] : mk(0.0, 0.0);
+                if (NRHS == 2) t1[k] = on1 ? p1t[l1] : mk(0.0, 0.0);
+                const bool on2 = ((U)(ls & 1) ^ hb) != 0;                 // bond (L-1, 0)
+                v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
+                if (NRHS == 2) t2[k] = on2 ? p2t[ls ^ 1] : mk(0.0, 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int ls = tid + k * kThreads;
+                const U s = base + (U)ls;
+                const U x = s ^ ((s >> 1) | ((s & (U)1) << (L - 1)));
+                const int na = (L <= 31) ? __popc((unsigned)x) : __popcll((unsigned long long)x);
+                const double d = qJ * (double)(L - 2 * na);
+                tile[ls] = v0[k];
+                q[k].x = fma(hJ, v1[k].x + v2[k].x, d * v0[k].x);
+                q[k].y = fma(hJ, v1[k].y + v2[k].y, d * v0[k].y);
+                if (NRHS == 2) {
+                    tile[TS + ls] = t0[k];
+                    qt[k].x = fma(hJ, t1[k].x + t2[k].x, d * t0[k].x);
+                    qt[k].y = fma(hJ, t1[k].y + t2[k].y, d * t0[k].y);
+                }
+            }
+        }
+        if (L - 1 > T) {
+            const U tbits = base >> T;   // bit (i - T) of tbits = site i, for i >= T
+            U act = (tbits ^ (tbits >> 1)) & ((((U)1) << (L - 1 - T)) - (U)1);   // bonds T..L-2
+            while (act) {
+                int bi[NB];
+#pragma unroll
+                for (int m = 0; m < NB; ++m) {
+                    bi[m] = -1;
+                    if (act) {
+                        const int pos = (L <= 31) ? __ffs((int)act) - 1 : __ffsll((long long)act) - 1;
+                        bi[m] = pos + T;
+                        act &= act - (U)1;
+                    }
+                }
+                cplx v[NB][PER], vt[NB][NRHS == 2 ? PER : 1];
+#pragma unroll
+                for (int m = 0; m < NB; ++m) {
+                    const U pb = base ^ ((U)3 << (bi[m] < 0 ? T : bi[m]));
+                    const cplx *pt = rv.at(pb);
+                    const cplx *ptt = NRHS == 2 ? tv.at(pb) : nullptr;
+#pragma unroll
+                    for (int k = 0; k < PER; ++k) {
+                        v[m][k] = bi[m] >= 0 ? pt[tid + k * kThreads] : mk(0.0, 0.0);
+                        if (NRHS == 2) vt[m][k] = bi[m] >= 0 ? ptt[tid + k * kThreads] : mk(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < NB; ++m)
+#pragma unroll
+                    for (int k = 0; k < PER; ++k) {
+                        q[k].x = fma(hJ, v[m][k].x, q[k].x);
+                        q[k].y = fma(hJ, v[m][k].y, q[k].y);
+                        if (NRHS == 2) { qt[k].x = fma(hJ, vt[m][k].x, qt[k].x); qt[k].y = fma(hJ, vt[m][k].y, qt[k].y); }
+                    }
+            }
+        }
+        __syncthreads();   // tile staged
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int ls = tid + k * kThreads;
+            const U s = base + (U)ls;
+            const U x = s ^ (s >> 1);   // bit i (< T-1): sites i, i+1 anti-aligned
+#pragma unroll
+            for (int i = 0; i < T - 1; ++i) {
+                if ((x >> i) & (U)1) {
+                    const cplx v = tile[ls ^ (3 << i)];
+                    q[k].x = fma(hJ, v.x, q[k].x);
+                    q[k].y = fma(hJ, v.y, q[k].y);
+                    if (NRHS == 2) {
+                        const cplx vt = tile[TS + (ls ^ (3 << i))];
+                        qt[k].x = fma(hJ, vt.x, qt[k].x);
+                        qt[k].y = fma(hJ, vt.y, qt[k].y);
+                    }
+                }
+            }
+            a.q[lbase + ls] = q[k];
+            if (NRHS == 2) {
+                a.qt[lbase + ls] = qt[k];
+                w = cfma_conj(tile[TS + ls], q[k], w);
+            } else {
+                w = cfma(tile[ls], q[k], w);
+            }
+        }
+    }
+    spmv_exit(a, kp, agent, w, sc);
+}
+
+template <int L>
+static cudaError_t launch_tiled(const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s) {
+    constexpr int T = kTileBits;
+    const size_t shm = sizeof(cplx) << T;
+    const bool p = a.st != nullptr;
+    if (a.bicg) {
+        static bool cfg = false;
+        if (!cfg) {
+            cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
+            cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
+            cfg = true;
+        }
+        if (kp.world > 1)
+            return launch_k(heisenberg_tiled_kernel<L, T, 2, true>, grid, kThreads, 2 * shm, s, p, a, kp, J);
+        return launch_k(heisenberg_tiled_kernel<L, T, 2, false>, grid, kThreads, 2 * shm, s, p, a, kp, J);
+    }
+    if (kp.world > 1)
+        return launch_k(heisenberg_tiled_kernel<L, T, 1, true>, grid, kThreads, shm, s, p, a, kp, J);
+    return launch_k(heisenberg_tiled_kernel<L, T, 1, false>, grid, kThreads, shm, s, p, a, kp, J);
+}
+
+}  // namespace sk
+
+#define SK_TILED_CASE(LL) case LL: return launch_tiled<LL>(a, kp, J, grid, s);
+#define SK_TILED_RANGE(NAME, CASES)                                                          \
+    namespace sk {                                                                           \
+    cudaError_t NAME(int L, const SpmvArgs &a, const KParams &kp, double J, int grid,        \
+                     cudaStream_t s) {                                                       \
+        switch (L) { CASES default: return cudaErrorInvalidValue; }                          \
+    }                                                                                        \
+    }

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kThreads, FULL ? 2 : 4)
 update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
     extern __shared__ cplx dyn[];  // FULL: coef[3 nz], flags[nz], list[nz]
     __shared__ ShiftScratch ss;
+    pdl_wait();
     DevState *st = kp.st;
     if (st->status != ST_ITERATING) return;
     if (blockIdx.x < kp.n_agents) {   // shift agents (a4 + a6 + pending a8), beside the streaming CTAs
@@ -246,6 +247,7 @@ update_proj_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restric
     __shared__ cplx rtile[kThreads];
     __shared__ cplx scratch[4 * (kThreads / 32)];
     __shared__ cplx lsum[32][1];
+    pdl_wait();
     DevState *st = kp.st;
     if (st->status != ST_ITERATING) return;
     if (blockIdx.x < kp.n_agents) {   // shift agents, beside the streaming CTAs
@@ -343,8 +345,8 @@ static cudaError_t launch_update_t(const KParams &kp, const cplx *q, const cplx 
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
         if (e != cudaSuccess) return e;
     }
-    update_kernel<NLMAX, BICG, FULL, R><<<kp.nblk_upd + kp.n_agents, kThreads, shm, s>>>(kp, q, qt);
-    return cudaGetLastError();
+    return launch_k(update_kernel<NLMAX, BICG, FULL, R>, kp.nblk_upd + kp.n_agents, kThreads, shm, s, true,
+                    kp, q, qt);
 }
 
 template <int NLMAX>
@@ -358,9 +360,9 @@ static cudaError_t launch_update_nl(const KParams &kp, const cplx *q, const cplx
 
 cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
     if (kp.nl > 4 && !kp.full) {
-        if (kp.bicg) update_proj_kernel<true><<<kp.nblk_upd + kp.n_agents, kThreads, 0, s>>>(kp, q, qt);
-        else update_proj_kernel<false><<<kp.nblk_upd + kp.n_agents, kThreads, 0, s>>>(kp, q, qt);
-        return cudaGetLastError();
+        if (kp.bicg)
+            return launch_k(update_proj_kernel<true>, kp.nblk_upd + kp.n_agents, kThreads, 0, s, true, kp, q, qt);
+        return launch_k(update_proj_kernel<false>, kp.nblk_upd + kp.n_agents, kThreads, 0, s, true, kp, q, qt);
     }
     if (kp.nl <= 1) return launch_update_nl<1>(kp, q, qt, s);
     if (kp.nl <= 4) return launch_update_nl<4>(kp, q, qt, s);
