@@ -12,7 +12,10 @@ a=b projection, COCG, complex128.
 Timing: W untimed iterations, then K iterations each bracketed by CUDA events on the solver's
 stream, with L2 flushed (256 MiB write) before every step outside the events; barrier +
 synchronize around the timed region; max over ranks.  Clocks are sampled with nvidia-smi
-during the timed region.  `--impl reference` times the CPU oracle (oracle/) on the same
+during the timed region.  `value` comes from a pass with nothing between the kernels; a second
+pass of the same K flushed steps records CUDA events around every kernel (on the solver's
+stream) for the per-kernel durations behind `roofline` (events between the kernels cost the
+programmatic-launch overlap, ~10 us per step at C2, so that pass is not the value).  `--impl reference` times the CPU oracle (oracle/) on the same
 workload (the reference arm of this tier: the paper has no code).
 """
 from __future__ import annotations
@@ -223,18 +226,18 @@ def main():
     if world > 1:
         skdist.connect(solver)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-    solver.profile_enable(True)
     with torch.cuda.stream(stream):
         solver.enqueue(args.warmup)
     torch.cuda.synchronize()
-    solver.profile(reset=True)
     launches0 = solver.profile()["launches"]
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+
+    def timed_pass(clk=None):
+        """K steps, L2 flushed before each (outside the events); returns the summed step ms."""
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         with torch.cuda.stream(stream):
             for i in range(args.steps):
                 flush.fill_(i & 0xff)
@@ -242,12 +245,21 @@ def main():
                 solver.enqueue(1)
                 ends[i].record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(step_ms))
+        if world > 1:
+            dist.barrier()
+        return float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+
+    # pass 1 (the value): no instrumentation between the kernels
+    with ClockSampler(local) as clk:
+        total_ms = timed_pass()
+    launches = solver.profile()["launches"] - launches0
+    # pass 2 (the kernel shares): the same K steps with CUDA events around each kernel on the
+    # solver's stream (the events cost the programmatic launch overlap, so not the value)
+    solver.profile_enable(True)
+    solver.profile(reset=True)
+    prof_total_ms = timed_pass()
     prof = solver.profile(reset=True)
-    launches = prof["launches"] - launches0
+    solver.profile_enable(False)
     coeffs = solver.coefficients()
     if world > 1:
         t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
@@ -277,6 +289,7 @@ def main():
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "ms_per_launch": per_launch_ms,
                      "peak_source": peak_src},
+        "profiled_pass_ms_per_step": prof_total_ms / args.steps,
         "kernel_ms_per_step": {k: v / max(prof["iterations"], 1) for k, v in
                                (("spmv", prof["ms_spmv"]), ("scalar", prof["ms_scalar"]),
                                 ("update", prof["ms_update"]))},

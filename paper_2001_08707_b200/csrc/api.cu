@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -169,6 +170,8 @@ static int enqueue_phase_a(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc, sk::S
     a.q = q_rc ? (cplx *)q_rc : c->kp.q;
     a.qt = q_rc ? (cplx *)qt_rc : c->kp.qt;
     a.part_w = c->kp.part_w;
+    a.work = c->kp.work;
+    a.grp = c->kp.grp;
     a.M = c->M;
     a.bicg = c->method == SK_BICG;
     CK(prof_mark(c));
@@ -361,7 +364,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.full = c->full;
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
-    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M)
+    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M, kp.bicg)
                    : (H->kind == SK_OP_RC ? sk::stream_blocks(M) : sk::csr_blocks(M));
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
     kp.n_agents = sk::shift_agents(c->nz);
@@ -388,12 +391,22 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
             if (kp.bicg) add(&kp.qt, vb);
         }
         add(&c->b, vb);
-        add(&kp.part_w, sizeof(cplx) * sk::kMaxSpmvBlocks);
+        {   // per-CTA partials, or the streaming SpMV's per-tile + per-group partials
+            int64_t np = sk::kMaxSpmvBlocks, ng = 1;
+            if (H->kind == SK_OP_HEISENBERG && sk::heis_stream(H->L, M, kp.bicg)) {
+                const int64_t nt = M >> sk::kTileBits;
+                np = std::max<int64_t>(np, sk::stream_partials(nt));
+                ng = std::max<int64_t>(1, (nt + sk::kStreamGroup - 1) / sk::kStreamGroup);
+            }
+            add(&kp.part_w, sizeof(cplx) * np);
+            add(&kp.grp, sizeof(uint32_t) * ng);
+        }
         add(&kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
         add(&zdev, sizeof(cplx) * c->nz);
         add(&kp.pibuf, sizeof(cplx) * 3 * c->nz);
         add(&kp.pi_frozen, sizeof(cplx) * c->nz);
         add(&kp.ticket, sizeof(uint32_t));
+        add(&kp.work, 2 * sizeof(unsigned long long));
         add(&kp.amin_part, sizeof(AminPart) * 8);
         add(&kp.active, c->nz);
         add(&kp.res, sizeof(double) * c->nz);
@@ -985,6 +998,17 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
     if (H->kind == SK_OP_HEISENBERG) {
         if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L)) return fail(SK_EINVAL, "L/M");
         a.M = H->M;
+        // tile queue of the streaming kernel: one zeroed pair per device, rewound by the kernel
+        // itself (stand-alone calls on one device must not run concurrently)
+        static unsigned long long *work[sk::kMaxWorld] = {};
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= sk::kMaxWorld) return fail(SK_EINVAL, "device ordinal");
+        if (!work[dev]) {
+            CK(cudaMalloc(&work[dev], 2 * sizeof(unsigned long long)));
+            CK(cudaMemset(work[dev], 0, 2 * sizeof(unsigned long long)));
+        }
+        a.work = work[dev];
         CK(sk::launch_heisenberg(a, KParams{}, H->L, H->J, s));
     } else if (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) {
         const int64_t M = H->M_local > 0 ? H->M_local : H->M;

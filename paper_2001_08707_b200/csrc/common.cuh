@@ -145,6 +145,8 @@ struct KParams {
     cplx *p, *x;         // [nz][M]
     int64_t *dbg_ts;     // optional [16] %globaltimer stamps
     uint32_t *ticket;    // [1] last-CTA detection in the SpMV kernel (reset by the last CTA)
+    unsigned long long *work;   // [2] tile queue of the streaming Heisenberg SpMV (reset by its last CTA)
+    uint32_t *grp;              // [ngroups] tile-group counters of the streaming SpMV (reset by their reducers)
     int32_t n_agents;    // shift-agent CTAs of the update kernel (each a slice of the shifts)
     struct AminPart *amin_part;   // [n_agents] per-agent argmin |pi_{n+1}| and survivor count
     // ---- multi-rank (world > 1): this rank owns global rows [row0, row0 + M); every rank's r

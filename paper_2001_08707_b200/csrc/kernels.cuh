@@ -32,10 +32,20 @@ constexpr int kThreads = 256;          // streaming kernels
 constexpr int kScalarThreads = 1024;   // the single-CTA init / finish kernel
 constexpr int kMaxBlocks = 148 * 8;    // grid cap for grid-stride streaming kernels
 constexpr int kMaxSpmvBlocks = 148 * 32;   // grid cap (= partial slots) of the SpMV kernels
+// w = <r, q> is reduced in a fixed order whatever CTA takes a tile: one partial per tile; up to
+// kStreamDirect tiles the seed CTA sums them all, beyond that the CTA completing a group of
+// kStreamGroup tiles sums the group (partials [ntiles, ntiles + ngroups) of part_w).
+constexpr int kStreamDirect = 4096;
+constexpr int kStreamGroup = 1024;
+inline __host__ __device__ int64_t stream_partials(int64_t ntiles) {
+    return ntiles <= kStreamDirect ? ntiles : ntiles + (ntiles + kStreamGroup - 1) / kStreamGroup;
+}
 constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
 
 int stream_blocks(int64_t M);
-int heisenberg_blocks(int L, int64_t M);        // worker CTAs (= partials) of the Heisenberg SpMV
+int heisenberg_blocks(int L, int64_t M, int bicg);   // worker CTAs (= partials) of the Heisenberg SpMV
+bool heis_stream(int L, int64_t M, int bicg);      // the TMA-fed streaming kernel is used
+int sm_count();
 int csr_blocks(int64_t M);                      // worker CTAs (= partials) of the CSR SpMV
 int update_blocks(int64_t M, int nl, int full, int nz); // worker CTAs (= partials) of the update
 int shift_agents(int nz);                        // shift-agent CTAs of the update
@@ -49,6 +59,8 @@ struct SpmvArgs {
     const cplx *t[3];
     cplx *q, *qt;
     cplx *part_w;
+    unsigned long long *work;   // [2] tile queue of the streaming Heisenberg SpMV (zero between launches)
+    uint32_t *grp;              // [ngroups] tile-group completion counters of the streaming SpMV
     int64_t M;
     int bicg;
 };

@@ -31,7 +31,34 @@ int stream_blocks(int64_t M) {
     return (int)b;
 }
 
-int heisenberg_blocks(int L, int64_t M) {
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+// The streaming (TMA-fed) kernel wins once the vector outgrows L2 (measured: L=24 215 vs 233 us,
+// L=26 0.98 vs 1.25 ms, L=28 4.8 vs 6.8 ms); below that the tiled kernel's shorter per-tile
+// latency chain wins (L=20 13.4 vs 14.6 us).  SHIFTK_HEIS_STREAM=0/1 forces either.
+bool heis_stream(int L, int64_t M, int bicg) {
+    static int en = -2;
+    if (en == -2) {
+        const char *e = getenv("SHIFTK_HEIS_STREAM");
+        en = !e ? -1 : (e[0] == '0' ? 0 : 1);
+    }
+    if (en == 0 || bicg || L <= kTileBits || L > 34 || M < (int64_t(1) << kTileBits)) return false;
+    return en == 1 || (M >> kTileBits) >= 8192;
+}
+
+int heisenberg_blocks(int L, int64_t M, int bicg) {
+    if (heis_stream(L, M, bicg)) {   // two CTAs per SM, one slot left for the finish agent
+        const int64_t ntiles = M >> kTileBits, slots = 2 * (int64_t)sm_count() - 1;
+        return (int)(ntiles < slots ? ntiles : slots);
+    }
     if (L > kTileBits && L <= 34 && M >= (int64_t(1) << kTileBits)) {
         const int64_t ntiles = M >> kTileBits;
         return (int)(ntiles < (int64_t)kMaxBlocks ? ntiles : (int64_t)kMaxBlocks);
@@ -94,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) heisenberg_kernel(SpmvArgs a, KParam
 }
 
 cudaError_t launch_heisenberg(const SpmvArgs &a, const KParams &kp, int L, double J, cudaStream_t s) {
-    const int workers = heisenberg_blocks(L, a.M);
+    const int workers = heisenberg_blocks(L, a.M, a.bicg);
     const int grid = workers + (a.st ? 1 : 0);
     if (a.M >= (int64_t(1) << kTileBits) && L > kTileBits && L <= 34) {
         if (L <= 16) return launch_tiled_a(L, a, kp, J, grid, s);

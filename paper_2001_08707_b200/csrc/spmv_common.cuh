@@ -55,11 +55,15 @@ static __device__ __forceinline__ bool spmv_enter(const SpmvArgs &a, bool &agent
     return true;
 }
 
+// `red`/`red_n`: the partials the last CTA reduces when the kernel wrote its own (fixed-order
+// per-tile / per-group partials of the streaming kernel); default: one partial per worker CTA.
 static __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParams &kp, bool agent, cplx w,
-                                          StepScratch &sc) {
-    __shared__ cplx scratch[kThreads / 32];
+                                          StepScratch &sc, const cplx *red = nullptr, int red_n = 0) {
+    __shared__ cplx scratch[32];
     __shared__ int last;
-    if (!agent && a.part_w) {
+    const bool per_cta = red == nullptr;
+    if (per_cta) { red = a.part_w; red_n = gridDim.x - 1; }
+    if (per_cta && !agent && a.part_w) {
         cplx v[1] = {w};
         block_sum<1>(v, scratch);
         if (threadIdx.x == 0) a.part_w[blockIdx.x - (a.st ? 1 : 0)] = v[0];
@@ -73,7 +77,7 @@ static __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParam
     dbg_stamp(kp.dbg_ts, 3);                                       // last CTA arrives
     __threadfence();
     if (kp.world > 1) {   // this rank's w only: the all-reduce and the seed step follow
-        reduce_columns(a.part_w, gridDim.x - 1, 1, 1, sc);
+        reduce_columns(red, red_n, 1, 1, sc);
         if (threadIdx.x == 0) {
             kp.wloc[0] = sc.col[0];
             *kp.ticket = 0u;
@@ -81,7 +85,7 @@ static __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParam
         return;
     }
     state_load_nosync(sc.S, kp.st);
-    reduce_columns(a.part_w, gridDim.x - 1, 1, 1, sc);   // (its barriers publish sc.S)
+    reduce_columns(red, red_n, 1, 1, sc);   // (its barriers publish sc.S)
     if (threadIdx.x == 0) {
         if (sc.S.status == ST_ITERATING) seed_step(&sc.S, sc.col[0], a.bicg, kp);
         *kp.ticket = 0u;

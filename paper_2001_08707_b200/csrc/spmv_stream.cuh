@@ -1,0 +1,295 @@
+// spmv_stream.cuh — the Heisenberg SpMV q = H r (COCG, one right-hand side) as a TMA-fed
+// streaming kernel.  Same decomposition as the tiled kernel (spmv_tiled.cuh): a tile is 2^T
+// consecutive basis states; the T-1 bonds inside a tile read the tile itself, the bond (T-1, T)
+// reads half of the tile that differs in bit T, the periodic bond (L-1, 0) the tile that differs
+// in bit L-1, and each ACTIVE tile-level bond i >= T (sites i, i+1 anti-aligned in the tile
+// index — uniform over the tile) the tile that differs in bits i and i+1 (P:L831 H, P:L508 bit
+// flips).  What changes is how the data moves:
+//   * one producer thread per CTA streams the tile and its partner tiles into shared memory
+//     with cp.async.bulk (global -> shared, mbarrier completion): a double-buffered own-tile
+//     slot and a ring of NS partner slots, so ~100 KB per CTA is in flight and the consumer
+//     warps never wait on an L2 round trip per element;
+//   * the tiles come from a dynamic queue (one 64-bit atomic per tile), so the CTAs, two per
+//     SM, stay busy until the last tile and concurrently processed tiles are adjacent in index
+//     (their partners across low tile bits are L2 hits);
+//   * 8 consumer warps accumulate q in registers (4 states per thread), then the internal bonds
+//     from the staged own tile, store q and the partial w = <r, q> (unconjugated, App. A).
+// Multi-rank (MULTI): the partner tile's address comes from the shard table — a bulk copy
+// straight from the owning rank's buffer (peer memory), fused into the same pipeline.
+#pragma once
+#include "spmv_common.cuh"
+
+namespace sk {
+
+constexpr int kStreamConsumers = 256;            // 8 consumer warps
+constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
+constexpr int kStreamSlots = 4;                  // partner ring depth (tiles)
+
+static __device__ __forceinline__ uint32_t sa(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void mb_init(uint64_t *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count) : "memory");
+}
+static __device__ __forceinline__ void mb_expect(uint64_t *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void mb_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
+static __device__ __forceinline__ void mb_wait(uint64_t *b, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(sa(b)), "r"(parity) : "memory");
+}
+static __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(b)) : "memory");
+}
+
+// active tile-level bonds T..L-2 of the tile with global first state `base` (bit j = bond j+T)
+template <int L, int T, typename U>
+static __device__ __forceinline__ U tile_bonds(U base) {
+    if (L - 1 <= T) return (U)0;
+    const U tbits = base >> T;
+    return (tbits ^ (tbits >> 1)) & ((((U)1) << (L - 1 - T)) - (U)1);
+}
+
+template <int L, int T, bool MULTI>
+__global__ void __launch_bounds__(kStreamThreads, 2)
+heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
+    constexpr int TS = 1 << T;
+    constexpr int NS = kStreamSlots;
+    constexpr int PER = TS / kStreamConsumers;
+    static_assert(PER * kStreamConsumers == TS, "tile must be a multiple of the consumer count");
+    using U = typename std::conditional<(L <= 31), uint32_t, uint64_t>::type;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    cplx *own = (cplx *)dsm;                       // [2][TS]
+    cplx *ring = own + 2 * TS;                     // [NS][TS]
+    __shared__ StepScratch sc;
+    __shared__ uint64_t own_full[2], own_empty[2], ring_full[NS], ring_empty[NS];
+    __shared__ int64_t tile_of[2];
+    __shared__ cplx wsm[2][kStreamConsumers / 32];
+    bool agent;
+    int buf;
+    if (!spmv_enter(a, agent, buf, sc, kp)) return;
+    const cplx *__restrict__ r = pick3(a.r, buf);
+    const RViewT<MULTI> rv = rview<MULTI>(r, kp.shard_r, buf, kp);
+    const int tid = threadIdx.x;
+    const int64_t ntiles = a.M >> T;
+    const U row0 = (U)(MULTI ? rv.row0 : 0);
+    cplx w = mk(0.0, 0.0);
+    if (!agent) {
+        if (tid == 0) {
+            for (int i = 0; i < 2; ++i) { mb_init(&own_full[i], 1); mb_init(&own_empty[i], kStreamConsumers / 32); }
+            for (int i = 0; i < NS; ++i) { mb_init(&ring_full[i], 1); mb_init(&ring_empty[i], kStreamConsumers / 32); }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();   // barriers initialised before anyone waits on them
+        if (tid >= kStreamConsumers) {
+            // ------------------------------------------------------------ producer lanes
+            // lane 0 takes tiles from the queue and loads the own tile; ring item `it` is issued
+            // by lane it % NS (several issuing lanes keep more bulk copies in flight per CTA)
+            const int pl = tid - kStreamConsumers;
+            if (pl < NS) {
+                constexpr unsigned pmask = (1u << NS) - 1u;
+                uint32_t it = 0;
+                int64_t ti_next = 0;
+                if (pl == 0) ti_next = (int64_t)atomicAdd(a.work, 1ull);
+                for (uint32_t j = 0;; ++j) {
+                    const int k = j & 1;
+                    const int64_t ti = __shfl_sync(pmask, ti_next, 0);
+                    if (pl == 0) mb_wait(&own_empty[k], ((j >> 1) & 1) ^ 1);
+                    if (ti >= ntiles) {
+                        if (pl == 0) {
+                            tile_of[k] = -1;
+                            mb_arrive(&own_full[k]);
+                        }
+                        break;
+                    }
+                    const U base = row0 + (U)(ti << T);
+                    if (pl == 0) {
+                        tile_of[k] = ti;
+                        mb_expect(&own_full[k], TS * sizeof(cplx));
+                        bulk_load(own + k * TS, rv.at(base), TS * sizeof(cplx), &own_full[k]);
+                    }
+                    // partner items, in the consumers' order
+                    const U tb = (base >> T) & (U)1;
+                    U act = tile_bonds<L, T, U>(base);
+                    for (int m = -2;; ++m) {
+                        const cplx *src;
+                        unsigned bytes = TS * sizeof(cplx);
+                        if (m == -2) {          // bond (T-1, T): the half with bit T-1 = tb
+                            src = rv.at(base ^ ((U)1 << T)) + ((int64_t)tb << (T - 1));
+                            bytes = (TS / 2) * sizeof(cplx);
+                        } else if (m == -1) {   // periodic bond (L-1, 0)
+                            src = rv.at(base ^ ((U)1 << (L - 1)));
+                        } else {
+                            if (!act) break;
+                            const int pos = (L <= 31) ? __ffs((int)act) - 1 : __ffsll((long long)act) - 1;
+                            act &= act - (U)1;
+                            src = rv.at(base ^ ((U)3 << (pos + T)));
+                        }
+                        const int s = it % NS;
+                        if (s == pl) {
+                            mb_wait(&ring_empty[s], ((it / NS) & 1) ^ 1);
+                            mb_expect(&ring_full[s], bytes);
+                            bulk_load(ring + s * TS, src, bytes, &ring_full[s]);
+                        }
+                        ++it;
+                    }
+                    // next tile: claimed once this tile's loads are all issued (the consumers
+                    // still have the last NS items to process)
+                    if (pl == 0) ti_next = (int64_t)atomicAdd(a.work, 1ull);
+                }
+            }
+        } else {
+            // ------------------------------------------------------------ consumers
+            const double qJ = 0.25 * J, hJ = 0.5 * J;
+            const int lane = tid & 31;
+            uint32_t it = 0;
+            for (uint32_t j = 0;; ++j) {
+                const int k = j & 1;
+                mb_wait(&own_full[k], (j >> 1) & 1);
+                const int64_t ti = tile_of[k];
+                if (ti < 0) break;
+                const cplx *ot = own + k * TS;
+                const U base = row0 + (U)(ti << T);
+                const U tb = (base >> T) & (U)1, hb = (base >> (L - 1)) & (U)1;
+                cplx v0[PER], q[PER];
+#pragma unroll
+                for (int e = 0; e < PER; ++e) {
+                    const int ls = tid + e * kStreamConsumers;
+                    const U s = base + (U)ls;
+                    const U x = s ^ ((s >> 1) | ((s & (U)1) << (L - 1)));
+                    const int na = (L <= 31) ? __popc((unsigned)x) : __popcll((unsigned long long)x);
+                    const double d = qJ * (double)(L - 2 * na);
+                    v0[e] = ot[ls];
+                    q[e] = mk(d * v0[e].x, d * v0[e].y);
+                }
+                U act = tile_bonds<L, T, U>(base);
+                for (int m = -2;; ++m) {
+                    if (m >= 0) {
+                        if (!act) break;
+                        act &= act - (U)1;
+                    }
+                    const int s = it % NS;
+                    mb_wait(&ring_full[s], (it / NS) & 1);
+                    const cplx *pt = ring + s * TS;
+#pragma unroll
+                    for (int e = 0; e < PER; ++e) {
+                        const int ls = tid + e * kStreamConsumers;
+                        bool on = true;
+                        cplx v;
+                        if (m == -2) {
+                            on = (((U)((ls >> (T - 1)) & 1)) ^ tb) != 0;
+                            v = pt[ls & (TS / 2 - 1)];
+                        } else if (m == -1) {
+                            on = (((U)(ls & 1)) ^ hb) != 0;
+                            v = pt[ls ^ 1];
+                        } else {
+                            v = pt[ls];
+                        }
+                        if (on) {
+                            q[e].x = fma(hJ, v.x, q[e].x);
+                            q[e].y = fma(hJ, v.y, q[e].y);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mb_arrive(&ring_empty[s]);
+                    ++it;
+                }
+                // bonds (i, i+1), i < T-1, inside the tile
+#pragma unroll
+                for (int e = 0; e < PER; ++e) {
+                    const int ls = tid + e * kStreamConsumers;
+                    const U s = base + (U)ls;
+                    const U x = s ^ (s >> 1);
+#pragma unroll
+                    for (int i = 0; i < T - 1; ++i) {
+                        if ((x >> i) & (U)1) {
+                            const cplx v = ot[ls ^ (3 << i)];
+                            q[e].x = fma(hJ, v.x, q[e].x);
+                            q[e].y = fma(hJ, v.y, q[e].y);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mb_arrive(&own_empty[k]);
+                cplx *qo = a.q + (ti << T);
+                cplx wt = mk(0.0, 0.0);
+#pragma unroll
+                for (int e = 0; e < PER; ++e) {
+                    qo[tid + e * kStreamConsumers] = q[e];
+                    wt = cfma(v0[e], q[e], wt);
+                }
+                if (a.part_w) {   // this tile's partial of w, fixed order
+                    wt = warp_sum(wt);
+                    if (lane == 0) wsm[k][tid >> 5] = wt;
+                    asm volatile("bar.sync 1, %0;" ::"n"(kStreamConsumers) : "memory");
+                    if (tid < 32) {
+                        bool reduce_group = false;
+                        if (tid == 0) {
+                            cplx v = wsm[k][0];
+#pragma unroll
+                            for (int m = 1; m < kStreamConsumers / 32; ++m) v = cadd(v, wsm[k][m]);
+                            a.part_w[ti] = v;
+                            if (ntiles > kStreamDirect) {
+                                const int64_t g = ti / kStreamGroup;
+                                const int64_t g0 = g * kStreamGroup;
+                                const uint32_t gn = (uint32_t)((ntiles - g0) < kStreamGroup ? (ntiles - g0) : kStreamGroup);
+                                __threadfence();
+                                reduce_group = atomicAdd(a.grp + g, 1u) == gn - 1u;
+                            }
+                        }
+                        reduce_group = __shfl_sync(0xffffffffu, reduce_group, 0);
+                        if (reduce_group) {   // sum the group's tile partials (lane-strided, tree)
+                            __threadfence();
+                            const int64_t g = ti / kStreamGroup, g0 = g * kStreamGroup;
+                            const int64_t g1 = (g0 + kStreamGroup) < ntiles ? g0 + kStreamGroup : ntiles;
+                            cplx v = mk(0.0, 0.0);
+                            for (int64_t i = g0 + lane; i < g1; i += 32) v = cadd(v, ldcg(a.part_w + i));
+                            v = warp_sum(v);
+                            if (lane == 0) {
+                                a.part_w[ntiles + g] = v;
+                                a.grp[g] = 0u;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        // queue bookkeeping: the last worker CTA rewinds the tile queue for the next launch
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            if (atomicAdd(a.work + 1, 1ull) == (unsigned long long)(gridDim.x - (a.st ? 1 : 0)) - 1ull) {
+                a.work[0] = 0ull;
+                a.work[1] = 0ull;
+            }
+        }
+    }
+    // the seed CTA reduces the per-tile (or per-group) partials in index order
+    const int64_t np = stream_partials(ntiles);
+    spmv_exit(a, kp, agent, w, sc, ntiles <= kStreamDirect ? a.part_w : a.part_w + ntiles,
+              (int)(ntiles <= kStreamDirect ? ntiles : np - ntiles));
+}
+
+template <int L>
+static cudaError_t launch_stream(const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s) {
+    constexpr int T = kTileBits;
+    const size_t shm = (size_t)(2 + kStreamSlots) * sizeof(cplx) << T;
+    static bool cfg = false;
+    if (!cfg) {
+        cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        cfg = true;
+    }
+    const bool p = a.st != nullptr;
+    if (kp.world > 1)
+        return launch_k(heisenberg_stream_kernel<L, T, true>, grid, kStreamThreads, shm, s, p, a, kp, J);
+    return launch_k(heisenberg_stream_kernel<L, T, false>, grid, kStreamThreads, shm, s, p, a, kp, J);
+}
+
+}  // namespace sk

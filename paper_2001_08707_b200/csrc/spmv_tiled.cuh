@@ -2,6 +2,7 @@
 // the instantiations are spread over spmv_tiled_*.cu so they compile in parallel).
 #pragma once
 #include "spmv_common.cuh"
+#include "spmv_stream.cuh"
 
 namespace sk {
 
@@ -151,6 +152,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
 template <int L>
 static cudaError_t launch_tiled(const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s) {
     constexpr int T = kTileBits;
+    if (a.work && heis_stream(L, a.M, a.bicg)) return launch_stream<L>(a, kp, J, grid, s);
     const size_t shm = sizeof(cplx) << T;
     const bool p = a.st != nullptr;
     if (a.bicg) {
