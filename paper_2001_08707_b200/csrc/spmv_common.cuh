@@ -86,6 +86,7 @@ static __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParam
     }
     state_load_nosync(sc.S, kp.st);
     reduce_columns(red, red_n, 1, 1, sc);   // (its barriers publish sc.S)
+    dbg_stamp(kp.dbg_ts, 9);                                       // partials reduced
     if (threadIdx.x == 0) {
         if (sc.S.status == ST_ITERATING) seed_step(&sc.S, sc.col[0], a.bicg, kp);
         *kp.ticket = 0u;

@@ -10,10 +10,18 @@ g = make_solver(to_device(p))
 g.run(20)
 names = {0: "spmv_worker1_start", 1: "agent_start", 2: "finish_done", 3: "last_cta", 4: "seed_done",
          5: "shift_agent_start", 6: "shift_done", 7: "upd_worker1_start", 8: "upd_lastcta_end",
-         9: "fin_reduced", 10: "fin_shiftloop", 11: "fin_switched", 12: "fin_compacted"}
+         9: "seed_reduced"}
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if "flush" in sys.argv else None
 for i in range(4):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if flush is not None:
+        flush.fill_(i)
+    a.record()
     g.enqueue(1)
+    b.record()
     torch.cuda.synchronize()
     ts = g.debug_timestamps()
     t0 = ts[0]
-    print({names[k]: int(ts[k] - t0) for k in range(13)})
+    d = {names[k]: int(ts[k] - t0) for k in range(10)}
+    d["event_step_ns"] = int(1e6 * a.elapsed_time(b))
+    print(d)
