@@ -7,6 +7,8 @@ the oracle never imports the product package; both take their inputs from ``synt
 Parity status of each oracle function:
   or_heisenberg_apply  pinned: Table 3 eigenvalues, ferromagnet, one-magnon waves
   or_csr_*_apply       pinned: scipy.sparse product on the same CSR arrays
+  or_heisenberg_sz_*   pinned: restriction of or_heisenberg_apply to the sector, dimension 924
+                       (P:L761), Table 3 from the sector alone; rank/unrank vs enumeration
   or_update (COCG)     pinned: dense solves, Lanczos continued fraction, pi = chi ratio,
                        collinearity, b^dagger r_n = 0, exact termination, sum rule
   or_update (BiCG)     pinned: dense solves, bi-orthogonality, BiCG == COCG on real H
@@ -84,6 +86,18 @@ def lib():
         L.or_x.restype = ctypes.c_void_p
         L.or_x.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.or_scalars.argtypes = [ctypes.c_void_p, _c128p]
+        L.or_sz_dim.restype = ctypes.c_int64
+        L.or_sz_dim.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.or_sz_states.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.or_heisenberg_sz_apply.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p,
+                                             ctypes.c_int64, _c128p, _c128p]
+        L.or_sz_rank.restype = ctypes.c_int64
+        L.or_sz_rank.argtypes = [ctypes.c_int, ctypes.c_int64]
+        L.or_sz_unrank.restype = ctypes.c_int64
+        L.or_sz_unrank.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64]
+        L.or_heisenberg_sz_row.restype = _C
+        L.or_heisenberg_sz_row.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, _c128p,
+                                           ctypes.c_int64]
     return _lib
 
 
@@ -107,6 +121,34 @@ def heisenberg_apply(L: int, J: float, r: np.ndarray) -> np.ndarray:
     return q
 
 
+def sz_dim(L: int, n: int) -> int:
+    return int(lib().or_sz_dim(L, n))
+
+
+def sz_states(L: int, n: int) -> np.ndarray:
+    """The sector basis: L-bit states with n up spins, ascending (R28)."""
+    out = np.empty(sz_dim(L, n), dtype=np.int64)
+    lib().or_sz_states(L, n, _ptr(out))
+    return out
+
+
+def sz_rank(L: int, s: int) -> int:
+    return int(lib().or_sz_rank(L, int(s)))
+
+
+def sz_unrank(L: int, n: int, rank: int) -> int:
+    return int(lib().or_sz_unrank(L, n, int(rank)))
+
+
+def heisenberg_sz_apply(L: int, n: int, J: float, r: np.ndarray) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.complex128)
+    st = sz_states(L, n)
+    assert r.shape[0] == st.shape[0]
+    q = np.empty_like(r)
+    lib().or_heisenberg_sz_apply(L, J, _ptr(st), st.shape[0], _ptr(r), _ptr(q))
+    return q
+
+
 def csr_apply(op: dict, r: np.ndarray) -> np.ndarray:
     r = np.ascontiguousarray(r, dtype=np.complex128)
     q = np.empty_like(r)
@@ -124,6 +166,8 @@ def apply_rows(op: dict, r: np.ndarray, rows) -> np.ndarray:
     for j, s in enumerate(rows):
         if op["kind"] == "heisenberg":
             v = L_.or_heisenberg_row(op["L"], op["J"], _ptr(r), int(s))
+        elif op["kind"] == "heisenberg_sz":
+            v = L_.or_heisenberg_sz_row(op["L"], op["n_up"], op["J"], _ptr(r), int(s))
         elif op["kind"] == "csr_real":
             v = L_.or_csr_real_row(_ptr(op["row_ptr"]), _ptr(op["col"]), _ptr(op["val"]), _ptr(r), int(s))
         else:
@@ -136,6 +180,8 @@ def apply_op(op: dict, r: np.ndarray) -> np.ndarray:
     """q = H r with the oracle's own operator code."""
     if op["kind"] == "heisenberg":
         return heisenberg_apply(op["L"], op["J"], r)
+    if op["kind"] == "heisenberg_sz":
+        return heisenberg_sz_apply(op["L"], op["n_up"], op["J"], r)
     return csr_apply(op, r)
 
 

@@ -485,3 +485,106 @@ void or_scalars(const or_state *st, cplx *out /* [6] */) {
     out[0] = st->alpha; out[1] = st->beta; out[2] = st->rho; out[3] = st->w;
     out[4] = st->zs; out[5] = st->alpha_prev;
 }
+
+/* ------------------------------------------------------------------ Sz sector (SURVEY f-3)
+
+   The Heisenberg chain conserves S^z_total, so H is block diagonal over sectors of fixed
+   number of up spins n (2 S^z = 2n - L; HPhi's "2Sz=0" sector, of dimension
+   C(L, L/2), e.g. 924 at L=12).  Sector basis (R28): the L-bit states with
+   popcount n in ASCENDING integer order; row i of the sector operator is the i-th such state.
+   The oracle builds that list by brute force and finds ranks by binary search; the rank by
+   counting (or_sz_rank) is only used for sampled rows at sizes where the list is too large. */
+
+/* number of states of the sector: C(L, n), by Pascal's rule */
+int64_t or_sz_dim(int L, int n) {
+    if (n < 0 || n > L) return 0;
+    int64_t c[65] = {0};
+    c[0] = 1;
+    for (int m = 1; m <= L; ++m)
+        for (int k = m; k >= 1; --k) c[k] += c[k - 1];
+    return c[n];
+}
+
+/* the sector states in ascending order (out has or_sz_dim(L, n) entries) */
+void or_sz_states(int L, int n, int64_t *out) {
+    int64_t i = 0;
+    for (int64_t s = 0; s < ((int64_t)1 << L); ++s)
+        if (__builtin_popcountll((unsigned long long)s) == n) out[i++] = s;
+}
+
+static int64_t sz_find(const int64_t *states, int64_t D, int64_t s) {
+    int64_t lo = 0, hi = D - 1;
+    while (lo <= hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (states[mid] == s) return mid;
+        if (states[mid] < s) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+/* q = H r restricted to the sector: the same bond sum as or_heisenberg_apply, on the list */
+void or_heisenberg_sz_apply(int L, double J, const int64_t *states, int64_t D, const cplx *r, cplx *q) {
+    for (int64_t a = 0; a < D; ++a) {
+        int64_t s = states[a];
+        cplx acc = 0;
+        for (int i = 0; i < L; ++i) {
+            int j = (i + 1) % L;
+            int bi = (int)((s >> i) & 1), bj = (int)((s >> j) & 1);
+            if (bi == bj) {
+                acc += 0.25 * J * r[a];
+            } else {
+                acc += -0.25 * J * r[a];
+                int64_t s2 = s ^ (((int64_t)1 << i) | ((int64_t)1 << j));
+                acc += 0.5 * J * r[sz_find(states, D, s2)];
+            }
+        }
+        q[a] = acc;
+    }
+}
+
+/* rank of s among the n-bit states by counting the smaller ones: scanning the set bits from the
+   top, a set bit at position p with m set bits at positions <= p contributes the C(p, m)
+   states that agree above p, have 0 at p and m set bits below p. */
+int64_t or_sz_rank(int L, int64_t s) {
+    int64_t rank = 0;
+    int m = __builtin_popcountll((unsigned long long)s);
+    for (int p = L - 1; p >= 0 && m > 0; --p) {
+        if ((s >> p) & 1) {
+            rank += or_sz_dim(p, m);
+            m -= 1;
+        }
+    }
+    return rank;
+}
+
+/* the state of rank `rank`: the inverse of the counting above, bit by bit from the top */
+int64_t or_sz_unrank(int L, int n, int64_t rank) {
+    int64_t s = 0;
+    int m = n;
+    for (int p = L - 1; p >= 0 && m > 0; --p) {
+        int64_t below = or_sz_dim(p, m);   /* states with a 0 here and m set bits below */
+        if (rank >= below) {
+            s |= (int64_t)1 << p;
+            rank -= below;
+            m -= 1;
+        }
+    }
+    return s;
+}
+
+/* one row of the sector operator (for sampled parity at large L) */
+cplx or_heisenberg_sz_row(int L, int n, double J, const cplx *r, int64_t a) {
+    int64_t s = or_sz_unrank(L, n, a);
+    cplx acc = 0;
+    for (int i = 0; i < L; ++i) {
+        int j = (i + 1) % L;
+        int bi = (int)((s >> i) & 1), bj = (int)((s >> j) & 1);
+        if (bi == bj) {
+            acc += 0.25 * J * r[a];
+        } else {
+            acc += -0.25 * J * r[a];
+            acc += 0.5 * J * r[or_sz_rank(L, s ^ (((int64_t)1 << i) | ((int64_t)1 << j)))];
+        }
+    }
+    return acc;
+}

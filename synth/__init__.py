@@ -20,7 +20,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = ["Problem", "CONFIGS", "make_problem", "spectrum_shifts", "contour_shifts",
-           "heisenberg_problem", "csr_real_problem", "lattice_problem"]
+           "heisenberg_problem", "heisenberg_sz_problem", "csr_real_problem", "lattice_problem"]
 
 
 @dataclasses.dataclass
@@ -81,6 +81,19 @@ def heisenberg_problem(name: str, L: int, seed: int, z: np.ndarray, *, J: float 
     return Problem(name=name, M=M, op={"kind": "heisenberg", "L": L, "J": float(J)}, b=b, z=z,
                    left=None, method="cocg", full_x=full_x, tol=tol, itermax=itermax,
                    meta={"L": L, "seed": seed})
+
+
+def heisenberg_sz_problem(name: str, L: int, n_up: int, seed: int, z: np.ndarray, *, J: float = 1.0,
+                          full_x: bool = False, tol: float = 1e-10, itermax: int = 20000) -> Problem:
+    """Heisenberg chain restricted to the sector of n_up up spins (rows = the
+    L-bit states with popcount n_up in ascending order, R28); b = normalised
+    PCG64(seed).standard_normal(C(L, n_up)), a = b."""
+    M = math.comb(L, n_up)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    b = _normalise(rng.standard_normal(M)).astype(np.complex128)
+    return Problem(name=name, M=M, op={"kind": "heisenberg_sz", "L": L, "J": float(J), "n_up": n_up},
+                   b=b, z=z, left=None, method="cocg", full_x=full_x, tol=tol, itermax=itermax,
+                   meta={"L": L, "n_up": n_up, "seed": seed})
 
 
 def csr_real_problem(name: str, M: int, seed: int, z: np.ndarray, *, n_match: int = 11,
@@ -209,6 +222,10 @@ CONFIGS = {
                W=8192, seed=3, nz=64, gamma=0.5, rho=0.25, n_left=32, tol=1e-10, itermax=50000),
     "c5": dict(desc="Heisenberg L=30, 512 shifts w+0.05i in [-16,4), COCG, a=b", L=30, seed=4,
                nz=512, w=(-16.0, 4.0), delta=0.05, full_x=False, tol=1e-10, itermax=20000),
+    # C5's chain in its largest sector (2Sz = 0, C(30,15) = 1.55e8 rows)
+    "c5sz": dict(desc="Heisenberg L=30 Sz=0 sector, 512 shifts w+0.05i in [-16,4), COCG, a=b",
+                 L=30, n_up=15, seed=4, nz=512, w=(-16.0, 4.0), delta=0.05, full_x=False,
+                 tol=1e-10, itermax=20000),
 }
 
 
@@ -224,6 +241,11 @@ def make_problem(name: str, **override) -> Problem:
         z = spectrum_shifts(cfg["nz"], cfg["w"][0], cfg["w"][1], cfg["delta"])
         return heisenberg_problem(tag, cfg["L"], cfg["seed"], z, full_x=cfg["full_x"],
                                   tol=cfg["tol"], itermax=cfg["itermax"])
+    if name == "c5sz":
+        z = spectrum_shifts(cfg["nz"], cfg["w"][0], cfg["w"][1], cfg["delta"])
+        n_up = cfg["n_up"] if "n_up" in override else cfg["L"] // 2
+        return heisenberg_sz_problem(tag, cfg["L"], n_up, cfg["seed"], z, full_x=cfg["full_x"],
+                                     tol=cfg["tol"], itermax=cfg["itermax"])
     if name == "c3":
         z = spectrum_shifts(cfg["nz"], cfg["w"][0], cfg["w"][1], cfg["delta"])
         return csr_real_problem(tag, cfg["M"], cfg["seed"], z, full_x=cfg["full_x"],

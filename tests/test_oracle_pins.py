@@ -458,3 +458,87 @@ def test_recalc_identity_and_new_shifts_vs_dense():
         exact = np.vdot(p.b, U @ (Ub / (z - lam)))
         assert abs(y2[k, 0] - exact) <= (res2[k] + 1e-12) / 0.05
     assert o.spmv_count == o.iterations     # recalc used no operator application
+
+
+# ------------------------------------------------------------------------------- Sz sector (f-3)
+
+def test_sz_sector_dimension():
+    """the L=12, Sz=0 sector has 924 states; the oracle's basis is the ascending list."""
+    assert oracle.sz_dim(12, 6) == 924
+    st = oracle.sz_states(12, 6)
+    assert st.size == 924 and np.all(np.diff(st) > 0)
+    assert np.all(popcount(st) == 6)
+    assert oracle.sz_dim(30, 15) == math.comb(30, 15)
+
+
+@pytest.mark.parametrize("L,n", [(10, 0), (10, 3), (10, 5), (11, 7), (12, 12)])
+def test_sz_rank_unrank_match_enumeration(L, n):
+    """The counting rank / unrank (used for sampled rows at large L) against brute-force order."""
+    st = oracle.sz_states(L, n)
+    for i, s in enumerate(st):
+        assert oracle.sz_rank(L, s) == i
+        assert oracle.sz_unrank(L, n, i) == s
+
+
+@pytest.mark.parametrize("L,n", [(10, 5), (10, 3), (11, 6), (9, 1)])
+def test_sz_apply_is_the_restriction_of_the_full_operator(L, n):
+    """H conserves S^z: the full-space product of a vector supported on the sector stays in the
+    sector and equals the sector product there (same per-row arithmetic: bit-exact)."""
+    rng = np.random.default_rng(L * 100 + n)
+    st = oracle.sz_states(L, n)
+    r = rng.standard_normal(st.size) + 1j * rng.standard_normal(st.size)
+    full = np.zeros(1 << L, dtype=np.complex128)
+    full[st] = r
+    qf = oracle.heisenberg_apply(L, 1.0, full)
+    qs = oracle.heisenberg_sz_apply(L, n, 1.0, r)
+    assert np.array_equal(qf[st], qs)
+    mask = np.ones(1 << L, dtype=bool)
+    mask[st] = False
+    assert np.all(qf[mask] == 0)
+
+
+def test_sz_sector_table3_from_the_sector_alone():
+    """Table 3 from the 924 x 924 sector operator built column by column."""
+    want = np.loadtxt(os.path.join(GOLDEN, "table3_heisenberg_L12.txt"))
+    D = oracle.sz_dim(12, 6)
+    H = np.empty((D, D))
+    e = np.zeros(D, dtype=np.complex128)
+    for j in range(D):
+        e[:] = 0
+        e[j] = 1
+        H[:, j] = oracle.heisenberg_sz_apply(12, 6, 1.0, e).real
+    assert np.array_equal(H, H.T)
+    ev = np.linalg.eigvalsh(H)[:7]
+    assert np.max(np.abs(ev - want)) < 1e-6
+
+
+def test_sz_sampled_rows_match_the_full_product():
+    """or_heisenberg_sz_row (counting rank, no list) = the list-based product, row by row."""
+    L, n = 12, 5
+    rng = np.random.default_rng(5)
+    D = oracle.sz_dim(L, n)
+    r = rng.standard_normal(D) + 1j * rng.standard_normal(D)
+    q = oracle.heisenberg_sz_apply(L, n, 1.0, r)
+    op = {"kind": "heisenberg_sz", "L": L, "n_up": n, "J": 1.0}
+    rows = [0, 1, 17, D // 2, D - 1]
+    assert np.array_equal(oracle.apply_rows(op, r, rows), q[rows])
+
+
+def test_sz_sector_solver_matches_dense_solve():
+    """Shifted COCG on the sector operator (the same oracle solver) converges to the dense
+    sector solve: y_k = b^dagger (z_k - H_sector)^-1 b."""
+    p = synth.make_problem("c5sz", L=10, nz=8)
+    D = p.M
+    H = np.empty((D, D))
+    e = np.zeros(D, dtype=np.complex128)
+    for j in range(D):
+        e[:] = 0
+        e[j] = 1
+        H[:, j] = oracle.heisenberg_sz_apply(10, 5, 1.0, e).real
+    o = oracle.solve(p)
+    assert o.status == oracle.CONVERGED
+    y = o.projections()[:, 0]
+    for k, zk in enumerate(p.z):
+        x = np.linalg.solve(zk * np.eye(D) - H, p.b)
+        yd = np.vdot(p.b, x)
+        assert abs(y[k] - yd) <= (p.tol + 1e-12) / abs(zk.imag)

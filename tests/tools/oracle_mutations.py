@@ -27,6 +27,9 @@ MUTATIONS = [
     ("int j = (i + 1) % L;", "int j = (i + 1 < L) ? i + 1 : i;"),        # periodic bond
     ("g[l] = dot_conj(st, st->left + l * st->M, v)",
      "g[l] = dot_plain(st, st->left + l * st->M, v)"),                    # a^dagger projection
+    ("if (rank >= below) {", "if (rank > below) {"),                     # sector unrank
+    ("rank += or_sz_dim(p, m);", "rank += or_sz_dim(p, m - 1);"),        # sector rank
+    ("acc += 0.25 * J * r[a];", "acc += 0.25 * J * r[s];"),              # sector row vs state
 ]
 
 
