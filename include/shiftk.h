@@ -52,7 +52,11 @@ enum sk_opkind {
                              the fly ("matrix elements are internally generated") */
     SK_OP_CSR_REAL = 1,   /* real-symmetric CSR, fp64 values                                   */
     SK_OP_CSR_CPLX = 2,   /* complex Hermitian CSR, complex128 values                          */
-    SK_OP_RC = 3          /* no operator: reverse communication only (sk_update_rc)            */
+    SK_OP_RC = 3,         /* no operator: reverse communication only (sk_update_rc)            */
+    SK_OP_HEISENBERG_SZ = 4 /* the chain of SK_OP_HEISENBERG restricted to the sector of n_up up
+                               spins (S^z conservation; HPhi's 2Sz sectors, dim 924
+                               at L=12, n_up=6).  Rows: the L-bit states with popcount
+                               n_up in ascending order (R28); M = C(L, n_up).  One GPU. */
 };
 
 /* Outcome of an iteration (returned through `status`, never as an error). */
@@ -100,6 +104,8 @@ typedef struct {
     const int64_t *row_ptr;
     const int32_t *col;
     const void *val;
+    int32_t n_up;        /* SK_OP_HEISENBERG_SZ: number of up spins, 0 <= n_up <= L              */
+    int32_t reserved;    /* zero                                                                 */
 } sk_operator;
 
 /* Solver parameters (the paper's *_init arguments, Alg. 1 P:L541 "init(ndim, nz, ndim,

@@ -179,6 +179,8 @@ static int enqueue_phase_a(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc, sk::S
         CK(sk::launch_rc_dot(a, c->kp, c->stream));
     else if (c->op.kind == SK_OP_HEISENBERG)
         CK(sk::launch_heisenberg(a, c->kp, c->op.L, c->op.J, c->stream));
+    else if (c->op.kind == SK_OP_HEISENBERG_SZ)
+        CK(sk::launch_heisenberg_sz(a, c->kp, c->op.L, c->op.n_up, c->op.J, c->stream));
     else
         CK(sk::launch_csr(a, c->kp, c->op.row_ptr, c->op.col, c->op.val, c->op.kind == SK_OP_CSR_CPLX,
                           c->avg_nnz, c->stream));
@@ -318,6 +320,15 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         case SK_OP_RC:
             if (M < 1) return fail(SK_EINVAL, "M");
             break;
+        case SK_OP_HEISENBERG_SZ: {
+            if (H->L < 1 || H->L > 34 || H->n_up < 0 || H->n_up > H->L)
+                return fail(SK_EINVAL, "Heisenberg sector: need 1 <= L <= 34, 0 <= n_up <= L");
+            int64_t dim = 1;   // C(L, n_up)
+            for (int j = 1; j <= H->n_up; ++j) dim = dim * (H->L - H->n_up + j) / j;
+            if (H->M != dim || M != H->M) return fail(SK_EINVAL, "Heisenberg sector: need M = C(L, n_up)");
+            if (world > 1) return fail(SK_EUNSUPPORTED, "Heisenberg sector operator with world > 1");
+            break;
+        }
         default:
             return fail(SK_EINVAL, "operator kind");
     }
@@ -365,7 +376,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
     kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M, kp.bicg)
-                   : (H->kind == SK_OP_RC ? sk::stream_blocks(M) : sk::csr_blocks(M));
+                   : ((H->kind == SK_OP_RC || H->kind == SK_OP_HEISENBERG_SZ) ? sk::stream_blocks(M)
+                                                                              : sk::csr_blocks(M));
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
@@ -1010,6 +1022,11 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
         }
         a.work = work[dev];
         CK(sk::launch_heisenberg(a, KParams{}, H->L, H->J, s));
+    } else if (H->kind == SK_OP_HEISENBERG_SZ) {
+        if (H->L < 1 || H->L > 34 || H->n_up < 0 || H->n_up > H->L || H->M < 1)
+            return fail(SK_EINVAL, "L/n_up/M");
+        a.M = H->M;
+        CK(sk::launch_heisenberg_sz(a, KParams{}, H->L, H->n_up, H->J, s));
     } else if (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) {
         const int64_t M = H->M_local > 0 ? H->M_local : H->M;
         if (!H->row_ptr || !H->col || !H->val || M < 1) return fail(SK_EINVAL, "CSR");

@@ -65,6 +65,7 @@ struct SpmvArgs {
     int bicg;
 };
 cudaError_t launch_heisenberg(const SpmvArgs &a, const KParams &kp, int L, double J, cudaStream_t s);
+cudaError_t launch_heisenberg_sz(const SpmvArgs &a, const KParams &kp, int L, int nup, double J, cudaStream_t s);
 // tiled Heisenberg SpMV by chain length: a 11..16, b 17..22, c 23..28, d 29..34 (spmv_tiled_*.cu)
 cudaError_t launch_tiled_a(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);
 cudaError_t launch_tiled_b(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libshiftk.so")
 
 COCG, BICG = 0, 1
-OP_HEISENBERG, OP_CSR_REAL, OP_CSR_CPLX, OP_RC = 0, 1, 2, 3
+OP_HEISENBERG, OP_CSR_REAL, OP_CSR_CPLX, OP_RC, OP_HEISENBERG_SZ = 0, 1, 2, 3, 4
 ITERATING, CONVERGED, MAXITER, BREAKDOWN = 0, 1, 2, 3
 STATUS_NAMES = {0: "iterating", 1: "converged", 2: "maxiter", 3: "breakdown"}
 MEM_HOST, MEM_DEVICE = 0, 1
@@ -49,7 +49,7 @@ class sk_operator(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("L", ctypes.c_int32), ("J", ctypes.c_double),
                 ("M", ctypes.c_int64), ("M_local", ctypes.c_int64), ("row_begin", ctypes.c_int64),
                 ("nnz", ctypes.c_int64), ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
-                ("val", ctypes.c_void_p)]
+                ("val", ctypes.c_void_p), ("n_up", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class sk_params(ctypes.Structure):
@@ -167,6 +167,8 @@ def make_operator(op: dict, M: int, dev_arrays: Optional[dict] = None, *, M_loca
         d = dev_arrays
         o.row_ptr, o.col, o.val = d["row_ptr"].data_ptr(), d["col"].data_ptr(), d["val"].data_ptr()
         o.nnz = int(d["col"].numel())
+    elif op["kind"] == "heisenberg_sz":
+        o.kind, o.L, o.J, o.n_up = OP_HEISENBERG_SZ, int(op["L"]), float(op["J"]), int(op["n_up"])
     elif op["kind"] == "rc":
         o.kind = OP_RC
     else:

@@ -50,7 +50,7 @@ def test_struct_layouts_match_header():
     from paper_2001_08707_b200 import shiftk
     # sizes fixed by the header's field order (natural alignment, x86-64)
     assert ctypes.sizeof(shiftk.sk_cplx) == 16
-    assert ctypes.sizeof(shiftk.sk_operator) == 4 + 4 + 8 + 8 * 4 + 8 * 3
+    assert ctypes.sizeof(shiftk.sk_operator) == 4 + 4 + 8 + 8 * 4 + 8 * 3 + 4 + 4
     assert ctypes.sizeof(shiftk.sk_params) == 4 + 4 + 8 + 8 + 8 + 4 + 4 + 8 + 8 + 4 + 4 + 8 + 8
     assert ctypes.sizeof(shiftk.sk_dist) == 16 + 16 + 8
 

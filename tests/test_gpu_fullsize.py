@@ -6,7 +6,7 @@ times, on what the oracle can afford there:
   scalar recurrences and seed switching still run over all 128 shifts);
 * C4 (8192^2 lattice, 64 contour points, 32 left vectors, BiCG): first iterations, all 64 x 32
   projections and residuals;
-* C5 (L = 30, 2^30 states): sampled rows of H r against the oracle's row routine, the
+* C5 (L = 30, 2^30 states) and its Sz = 0 sector (f-3): sampled rows of H r against the oracle's row routine, the
   ferromagnet H 1 = (L/4) 1 bit-exactly, and exact termination after 3 iterations for a
   right-hand side with 3 distinct energies (closed-form G(z)) — properties that hold at any size.
 """
@@ -132,3 +132,23 @@ def test_c5_full_size_operator_and_exact_termination():
     assert np.max(res) < 1e-10
     # rigorous bound |G_n - G| <= ||r^(k)|| / |Im z| (rounding of psi_F dominates at L = 30)
     assert np.all(np.abs(g.projections()[:, 0] - Gex) <= res / 0.05 + 1e-13)
+
+
+def test_c5sz_full_size_sector_operator_sampled_rows():
+    """The L = 30 chain in its Sz = 0 sector (f-3, C(30,15) = 155,117,520 rows): sampled rows of
+    H r (GPU combinatorial ranking) against the oracle's counting-rank row routine, including
+    the first and last rows and rows whose periodic bond is active."""
+    L, n = 30, 15
+    D = math.comb(L, n)
+    rng = np.random.default_rng(30)
+    r = rng.standard_normal(D) + 1j * rng.standard_normal(D)
+    op = shiftk.make_operator({"kind": "heisenberg_sz", "L": L, "J": 1.0, "n_up": n}, D)
+    rd = torch.from_numpy(r).cuda()
+    qd = torch.empty_like(rd)
+    shiftk.apply_operator(op, rd, qd)
+    torch.cuda.synchronize()
+    rows = [0, 1, 2, D // 3, D // 2, D - 2, D - 1] + list(rng.integers(0, D, 40))
+    q_rows = qd[torch.tensor(rows, device="cuda")].cpu().numpy()
+    del qd, rd
+    qo = oracle.apply_rows({"kind": "heisenberg_sz", "L": L, "n_up": n, "J": 1.0}, r, rows)
+    assert np.max(np.abs(q_rows - qo) / np.maximum(np.abs(qo), 1e-300)) <= 1e-13

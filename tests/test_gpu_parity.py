@@ -88,6 +88,26 @@ def test_heisenberg_operator_parity(L):
     assert np.max(np.abs(qd.cpu().numpy() - qo)) <= 1e-14 * np.max(np.abs(qo))
 
 
+@pytest.mark.parametrize("L,n", [(12, 6), (16, 8), (14, 3), (11, 0), (20, 10)])
+def test_heisenberg_sz_operator_parity(L, n):
+    """Sector operator (f-3): GPU combinatorial ranking vs the oracle's enumerated basis."""
+    rng = np.random.default_rng(L * 7 + n)
+    D = oracle.sz_dim(L, n)
+    r = rng.standard_normal(D) + 1j * rng.standard_normal(D)
+    op = shiftk.make_operator({"kind": "heisenberg_sz", "L": L, "J": 1.0, "n_up": n}, D)
+    rd = torch.from_numpy(r).cuda()
+    qd = torch.empty_like(rd)
+    shiftk.apply_operator(op, rd, qd)
+    torch.cuda.synchronize()
+    qo = oracle.heisenberg_sz_apply(L, n, 1.0, r)
+    assert np.max(np.abs(qd.cpu().numpy() - qo)) <= 1e-14 * np.max(np.abs(qo))
+
+
+def test_heisenberg_sz_window():
+    """Trajectory window on the Sz = 0 sector of a 16-site chain (C(16,8) = 12870 rows)."""
+    run_window(synth.make_problem("c5sz", L=16, nz=64), 20)
+
+
 def test_heisenberg_ferromagnet_bit_exact_gpu():
     L = 20
     op = shiftk.make_operator({"kind": "heisenberg", "L": L, "J": 1.0}, 1 << L)
