@@ -20,7 +20,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = ["Problem", "CONFIGS", "make_problem", "spectrum_shifts", "contour_shifts",
-           "heisenberg_problem", "heisenberg_sz_problem", "csr_real_problem", "lattice_problem"]
+           "heisenberg_problem", "heisenberg_sz_problem", "ss_inputs", "csr_real_problem", "lattice_problem"]
 
 
 @dataclasses.dataclass
@@ -94,6 +94,18 @@ def heisenberg_sz_problem(name: str, L: int, n_up: int, seed: int, z: np.ndarray
     return Problem(name=name, M=M, op={"kind": "heisenberg_sz", "L": L, "J": float(J), "n_up": n_up},
                    b=b, z=z, left=None, method="cocg", full_x=full_x, tol=tol, itermax=itermax,
                    meta={"L": L, "n_up": n_up, "seed": seed})
+
+
+def ss_inputs(L: int = 12, n_up: int = 6, n_l: int = 5, seed: int = 7, gamma: float = -5.0,
+              rho: float = 0.8, n_z: int = 100):
+    """Inputs of the contour-integral example (Table 3): the
+    sector operator, N_l source vectors phi_l with i.i.d. standard normal entries (drawn from
+    PCG64(seed) as one [n_l, C(L, n_up)] array; R29), and the contour points."""
+    D = math.comb(L, n_up)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    phis = rng.standard_normal((n_l, D)).astype(np.complex128)
+    op = {"kind": "heisenberg_sz", "L": L, "J": 1.0, "n_up": n_up}
+    return op, phis, contour_shifts(n_z, gamma, rho)
 
 
 def csr_real_problem(name: str, M: int, seed: int, z: np.ndarray, *, n_match: int = 11,

@@ -30,16 +30,27 @@ MUTATIONS = [
     ("if (rank >= below) {", "if (rank > below) {"),                     # sector unrank
     ("rank += or_sz_dim(p, m);", "rank += or_sz_dim(p, m - 1);"),        # sector rank
     ("acc += 0.25 * J * r[a];", "acc += 0.25 * J * r[s];"),              # sector row vs state
+    # contour-integral eigensolver (oracle/ss.py)
+    ("s += (z[j] - gamma) / n_z * (z[j] - gamma) ** k * X[l, j]",
+     "s += 1.0 / n_z * (z[j] - gamma) ** k * X[l, j]", "ss.py"),        # dz weight
+    ("s += (z[j] - gamma) / n_z * (z[j] - gamma) ** k * X[l, j]",
+     "s += (z[j] - gamma) / n_z * (z[j] - gamma) ** (k + 1) * X[l, j]", "ss.py"),   # moment order
+    ("Ht = Ut.conj().T @ HU", "Ht = Ut.T @ HU", "ss.py"),               # Rayleigh-Ritz conj
 ]
 
 
 def main():
-    orig = open(SRC).read()
     survived = []
-    try:
-        for a, b in MUTATIONS:
-            assert a in orig, a
-            open(SRC, "w").write(orig.replace(a, b, 1))
+    only = os.environ.get("MUTATIONS_ONLY")   # e.g. "ss.py": just the mutations of that file
+    for m in MUTATIONS:
+        if only and (m[2] if len(m) > 2 else "shiftk_oracle.c") != only:
+            continue
+        a, b = m[0], m[1]
+        src = os.path.join(ROOT, "oracle", m[2]) if len(m) > 2 else SRC
+        orig = open(src).read()
+        assert a in orig, a
+        try:
+            open(src, "w").write(orig.replace(a, b, 1))
             r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q",
                                 os.path.join(ROOT, "tests", "test_oracle_pins.py")],
                                cwd=ROOT, capture_output=True, text=True)
@@ -47,9 +58,9 @@ def main():
             print(("caught   " if caught else "SURVIVED ") + a + "  ->  " + b, flush=True)
             if not caught:
                 survived.append(a)
-    finally:
-        open(SRC, "w").write(orig)
-        os.utime(SRC)
+        finally:
+            open(src, "w").write(orig)
+            os.utime(src)
     sys.exit(1 if survived else 0)
 
 
