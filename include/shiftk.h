@@ -226,6 +226,26 @@ int sk_finalize(sk_ctx **ctx);
    tests.  stream: cudaStream_t or NULL (default stream). */
 int sk_apply_operator(const sk_operator *H, const sk_cplx *r_dev, sk_cplx *q_dev, void *stream);
 
+/* ---- contour-integral eigensolver building blocks ----------
+   The moments s_k = (1/2 pi i) oint (z - z0)^k (z - H)^{-1} phi dz are linear
+   combinations of the full-mode solutions x^(j) of one solver (sk_get_solution) with the
+   trapezoidal weights of the contour points z_j; the Rayleigh-Ritz step
+   needs the Gram matrices S^dagger S and U~^dagger H U~.  The small eigenproblems are the
+   caller's (host).
+
+   out[c][i] = sum_j W[j * n_out + c] * X[j * ld_x + i] for 0 <= c < n_out, 0 <= i < M.
+   X: DEVICE, n_in rows of stride ld_x >= M (e.g. the solutions of one context: ld_x =
+   sk_get_solution(k+1) - sk_get_solution(k)); W: HOST [n_in][n_out] (copied); out: DEVICE
+   [n_out][M], must not alias X.  Returns after the result is complete (synchronises `stream`).
+   SK_EINVAL on null pointers or sizes (n_out <= 4096). */
+int sk_combine(const sk_cplx *X, int64_t n_in, int64_t ld_x, int64_t M, const sk_cplx *W, int64_t n_out,
+               sk_cplx *out, void *stream);
+
+/* G[a * nb + b] = sum_i conj(A[a * M + i]) * B[b * M + i] (fixed summation order, deterministic).
+   A: DEVICE [na][M], B: DEVICE [nb][M], G: HOST [na][nb]; 1 <= na, nb <= 64.  Synchronous on
+   `stream`.  SK_EINVAL on null pointers or sizes. */
+int sk_gram(const sk_cplx *A, int64_t na, const sk_cplx *B, int64_t nb, int64_t M, sk_cplx *G, void *stream);
+
 /* Human-readable text of the last error on this thread (never NULL). */
 const char *sk_last_error(void);
 

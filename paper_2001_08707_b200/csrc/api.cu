@@ -27,6 +27,9 @@ static int fail(int code, const std::string &msg) {
     return code;
 }
 
+// error reporting for the other translation units (contour.cu)
+int sk_set_error(int code, const char *msg) { return fail(code, msg); }
+
 #define CK(call)                                                                                 \
     do {                                                                                         \
         cudaError_t e_ = (call);                                                                 \

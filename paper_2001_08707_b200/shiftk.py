@@ -32,7 +32,7 @@ EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_ru
            "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
            "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
            "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc", "sk_checkpoint",
-           "sk_restore"]
+           "sk_restore", "sk_combine", "sk_gram"]
 
 
 class ShiftkError(RuntimeError):
@@ -105,6 +105,8 @@ def load(path: str = LIB_PATH):
         "sk_get_coefficients": [VP, P(sk_coeffs)],
         "sk_finalize": [P(VP)],
         "sk_apply_operator": [P(sk_operator), VP, VP, VP],
+        "sk_combine": [VP, I64, I64, I64, VP, I64, VP, VP],
+        "sk_gram": [VP, I64, VP, I64, I64, VP, VP],
         "sk_profile_enable": [VP, I32],
         "sk_copy_solution": [VP, I64, VP, I32],
         "sk_debug_timestamps": [VP, VP],
@@ -194,6 +196,24 @@ def apply_operator(op: sk_operator, r_dev, q_dev, stream: int = 0):
     """q = H r on device tensors (complex128)."""
     _check(load().sk_apply_operator(ctypes.byref(op), r_dev.data_ptr(), q_dev.data_ptr(),
                                     ctypes.c_void_p(stream)), "sk_apply_operator")
+
+
+def combine(X_ptr: int, n_in: int, ld_x: int, M: int, W: np.ndarray, out_dev, stream: int = 0):
+    """out[c] = sum_j W[j, c] X[j] (device rows of stride ld_x; W host [n_in, n_out])."""
+    W = np.ascontiguousarray(W, dtype=np.complex128)
+    assert W.shape[0] == n_in
+    _check(load().sk_combine(X_ptr, n_in, ld_x, M, W.ctypes.data, W.shape[1], out_dev.data_ptr(),
+                             ctypes.c_void_p(stream)), "sk_combine")
+
+
+def gram(A_dev, B_dev, stream: int = 0) -> np.ndarray:
+    """A^dagger B for device row blocks A [na, M], B [nb, M] (host result [na, nb])."""
+    na, M = A_dev.shape
+    nb = B_dev.shape[0]
+    G = np.empty((na, nb), dtype=np.complex128)
+    _check(load().sk_gram(A_dev.data_ptr(), na, B_dev.data_ptr(), nb, M, G.ctypes.data,
+                          ctypes.c_void_p(stream)), "sk_gram")
+    return G
 
 
 class Group:
