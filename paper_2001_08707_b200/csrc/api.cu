@@ -408,12 +408,21 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&c->b, vb);
         {   // per-CTA partials, or the streaming SpMV's per-tile + per-group partials
             int64_t np = sk::kMaxSpmvBlocks, ng = 1;
+            // the w partials the seed step reduces: [wred_off, wred_off + wred_n) of a half
+            kp.wred_off = 0;
+            kp.wred_n = kp.nblk_spmv;
             if (H->kind == SK_OP_HEISENBERG && sk::heis_stream(H->L, M, kp.bicg)) {
                 const int64_t nt = M >> sk::kTileBits;
                 np = std::max<int64_t>(np, sk::stream_partials(nt));
                 ng = std::max<int64_t>(1, (nt + sk::kStreamGroup - 1) / sk::kStreamGroup);
+                kp.wred_off = nt <= sk::kStreamDirect ? 0 : nt;
+                kp.wred_n = (int32_t)(nt <= sk::kStreamDirect ? nt : ng);
             }
-            add(&kp.part_w, sizeof(cplx) * np);
+            // deferred seed step on one GPU with the built-in operator: two halves (iteration
+            // parity), because the next SpMV writes its partials while the finish reads these
+            kp.defer = (world == 1 && H->kind != SK_OP_RC) ? 1 : 0;
+            kp.wred_stride = np;
+            add(&kp.part_w, sizeof(cplx) * np * 2);
             add(&kp.grp, sizeof(uint32_t) * ng);
         }
         add(&kp.part_u, sizeof(cplx) * sk::kMaxBlocks * (2 + c->nl));
@@ -582,7 +591,7 @@ struct CkptHeader {
     int64_t M, nz, nl, world, rank;
     int32_t method, full;
 };
-static const uint64_t kCkptMagic = 0x314b5054504b4b53ull;   // "SKKPTPK1"
+static const uint64_t kCkptMagic = 0x324b5054504b4b53ull;   // "SKKPTPK2"
 
 int sk_checkpoint(sk_ctx *c, void *buf, size_t *bytes) {
     if (!c || !bytes) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");

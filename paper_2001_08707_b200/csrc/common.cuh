@@ -89,6 +89,12 @@ __host__ __device__ __forceinline__ T pick3(T const (&a)[3], int64_t i) {
 // buffers' scale factors, never their elements (O(1) instead of O(N_z)).
 // Retirement after a finish is applied lazily by the next per-shift pass (lz_pending).
 // ---------------------------------------------------------------------------------------------
+// Seed scalars of one iteration (steps.cuh seed_compute).
+struct SeedOut {
+    cplx w, alpha, beta, c, a_cur, a_q, a_prev, sr;
+    int32_t ok, pad_;
+};
+
 struct DevState {
     int64_t n;           // completed iterations
     int64_t n_started;   // iterations whose seed scalars were computed
@@ -115,6 +121,16 @@ struct DevState {
     double nu;           // ||r_n||_2 (true scale)
     double tol;
     int64_t itermax;
+    int64_t seq;         // iterations whose update ran: the SpMV reads r[seq % 3] and writes its w
+                         // partials to half (seq & 1) of part_w (written only by the update kernel)
+    // the parts of the next seed step that do not depend on w, evaluated by the finish that
+    // fixed rho_n (so the seed step on the critical path is one complex division):
+    cplx beta_nx;        // beta_{n-1} = rho_n / rho_{n-1}   (0 at n = 0)
+    cplx gamma_nx;       // beta_{n-1} / alpha_{n-1}          (0 at n = 0)
+    int32_t rho_small;   // |rho_n| < 1e-300 (R12)
+    int32_t pad2_;
+    SeedOut rec;         // deferred mode: the seed scalars the update kernel used (committed by
+                         // the next finish; written only by the update kernel's CTA 0)
 };
 
 // Pointers/sizes passed by value to every kernel.
@@ -129,9 +145,15 @@ struct KParams {
     cplx *t[3];          // shadow (BiCG)
     cplx *q, *qt;        // H r, H t (raw, i.e. applied to stored vectors)
     const cplx *left;    // [nl][M] (== b when a = b)
-    cplx *part_w;        // [nblk_spmv]
+    cplx *part_w;        // [2][wred_stride]: SpMV w partials, half (seq & 1) per iteration
     cplx *part_u;        // [nblk_upd][2 + nl]
     int32_t nblk_spmv, nblk_upd;   // worker CTAs (= partial count) of the SpMV / update kernels
+    // deferred seed step (world == 1, built-in operator): the update CTAs evaluate the seed
+    // scalars themselves from the w partials [wred_off, wred_off + wred_n) of the current half;
+    // the next finish commits them to the state (steps.cuh agent_finish)
+    int32_t defer;
+    int32_t wred_n;
+    int64_t wred_off, wred_stride;
     // per-shift arrays [nz]
     const cplx *z;
     cplx *pibuf;         // [3][nz] rotating pi_n^k

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(kThreads) scalar_kernel(KParams kp, int phase)
         }
         if (threadIdx.x == 0) {
             sc.S.rho_cur = sc.col[0];
+            seed_prepare(&sc.S);
             sc.S.nu = nu;
             sc.S.n_active = kp.nz;
             sc.S.lz_pending = 0;
@@ -36,7 +37,7 @@ __global__ void __launch_bounds__(kThreads) scalar_kernel(KParams kp, int phase)
     // test that the finish of the previous iteration left pending (the state is read via L2)
     const int pending = __ldcg(&kp.st->pending);
     if (pending) {
-        finish_step(kp, sc, /*eager=*/true);
+        agent_finish(kp, sc, /*eager=*/true);
     } else if (__ldcg(&kp.st->status) == ST_BREAKDOWN && __ldcg(&kp.st->lz_pending)) {
         state_load_nosync(sc.S, kp.st);
         __syncthreads();

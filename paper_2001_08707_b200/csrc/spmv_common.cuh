@@ -44,12 +44,12 @@ static __device__ __forceinline__ bool spmv_enter(const SpmvArgs &a, bool &agent
     pdl_wait();
     if (!a.st) return true;
     if (a.st->status != ST_ITERATING) return false;
-    buf = (int)(a.st->n_started % 3);
+    buf = (int)(a.st->seq % 3);   // (seq is written only by the update kernel)
     if (blockIdx.x == 1) dbg_stamp(kp.dbg_ts, 0);                 // first worker CTA starts
     if (blockIdx.x == 0) {
         agent = true;
         dbg_stamp(kp.dbg_ts, 1);
-        if (a.st->pending) finish_step(kp, sc, /*eager=*/false);
+        if (a.st->pending) agent_finish(kp, sc, /*eager=*/false);
         dbg_stamp(kp.dbg_ts, 2);                                   // finish agent done
     }
     return true;
@@ -62,13 +62,16 @@ static __device__ __forceinline__ void spmv_exit(const SpmvArgs &a, const KParam
     __shared__ cplx scratch[32];
     __shared__ int last;
     const bool per_cta = red == nullptr;
-    if (per_cta) { red = a.part_w; red_n = gridDim.x - 1; }
-    if (per_cta && !agent && a.part_w) {
+    // deferred seed step: this iteration's half of part_w; the update CTAs reduce it
+    cplx *pw = a.part_w;
+    if (a.st && kp.defer && pw) pw += (a.st->seq & 1) * kp.wred_stride;
+    if (per_cta) { red = pw; red_n = gridDim.x - 1; }
+    if (per_cta && !agent && pw) {
         cplx v[1] = {w};
         block_sum<1>(v, scratch);
-        if (threadIdx.x == 0) a.part_w[blockIdx.x - (a.st ? 1 : 0)] = v[0];
+        if (threadIdx.x == 0) pw[blockIdx.x - (a.st ? 1 : 0)] = v[0];
     }
-    if (!a.st) return;
+    if (!a.st || kp.defer) return;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = (atomicAdd(kp.ticket, 1u) == gridDim.x - 1);

@@ -79,6 +79,7 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
     const int tid = threadIdx.x;
     const int64_t ntiles = a.M >> T;
     const U row0 = (U)(MULTI ? rv.row0 : 0);
+    cplx *const pw = (a.part_w && a.st && kp.defer) ? a.part_w + (a.st->seq & 1) * kp.wred_stride : a.part_w;
     cplx w = mk(0.0, 0.0);
     if (!agent) {
         if (tid == 0) {
@@ -224,7 +225,7 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
                     qo[tid + e * kStreamConsumers] = q[e];
                     wt = cfma(v0[e], q[e], wt);
                 }
-                if (a.part_w) {   // this tile's partial of w, fixed order
+                if (pw) {   // this tile's partial of w, fixed order
                     wt = warp_sum(wt);
                     if (lane == 0) wsm[k][tid >> 5] = wt;
                     asm volatile("bar.sync 1, %0;" ::"n"(kStreamConsumers) : "memory");
@@ -234,7 +235,7 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
                             cplx v = wsm[k][0];
 #pragma unroll
                             for (int m = 1; m < kStreamConsumers / 32; ++m) v = cadd(v, wsm[k][m]);
-                            a.part_w[ti] = v;
+                            pw[ti] = v;
                             if (ntiles > kStreamDirect) {
                                 const int64_t g = ti / kStreamGroup;
                                 const int64_t g0 = g * kStreamGroup;
@@ -249,10 +250,10 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
                             const int64_t g = ti / kStreamGroup, g0 = g * kStreamGroup;
                             const int64_t g1 = (g0 + kStreamGroup) < ntiles ? g0 + kStreamGroup : ntiles;
                             cplx v = mk(0.0, 0.0);
-                            for (int64_t i = g0 + lane; i < g1; i += 32) v = cadd(v, ldcg(a.part_w + i));
+                            for (int64_t i = g0 + lane; i < g1; i += 32) v = cadd(v, ldcg(pw + i));
                             v = warp_sum(v);
                             if (lane == 0) {
-                                a.part_w[ntiles + g] = v;
+                                pw[ntiles + g] = v;
                                 a.grp[g] = 0u;
                             }
                         }
@@ -272,7 +273,7 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
     }
     // the seed CTA reduces the per-tile (or per-group) partials in index order
     const int64_t np = stream_partials(ntiles);
-    spmv_exit(a, kp, agent, w, sc, ntiles <= kStreamDirect ? a.part_w : a.part_w + ntiles,
+    spmv_exit(a, kp, agent, w, sc, ntiles <= kStreamDirect ? pw : pw + ntiles,
               (int)(ntiles <= kStreamDirect ? ntiles : np - ntiles));
 }
 

@@ -216,6 +216,8 @@ static __device__ void retire_pass(const KParams &kp, StepScratch &sc) {
 }
 
 // ------------------------------------------------------------------------------- finish_step
+static __device__ __forceinline__ void seed_prepare(DevState *S);
+
 // Finishes iteration m = S->n (pending): consumes the update partials of r_{m+1} and the
 // argmin of |pi_{m+1}| found by the shift step of iteration m.  O(1) work besides the partial
 // reduction: the switch rescales buffer scale factors, and the retirement test is left pending
@@ -223,14 +225,15 @@ static __device__ void retire_pass(const KParams &kp, StepScratch &sc) {
 // with the LARGEST |pi| (res = nu/|pi| < tol), so the argmin over the survivors is the argmin
 // over the shifts active before the test unless every shift retires — which is exactly the
 // test nu/|pi_{s*}| < tol on that argmin (R10, R11).
-static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eager) {
-    state_load_nosync(sc.S, kp.st);
+static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eager, bool loaded = false) {
+    if (!loaded) state_load_nosync(sc.S, kp.st);
     DevState *S = &sc.S;
     const int nl = kp.nl, nred = 2 + nl;
     if (kp.usum) reduce_columns(kp.usum, 1, nred, nred, sc);         // all-reduced (world > 1)
     else reduce_columns(kp.part_u, kp.nblk_upd, nred, nred, sc);   // (barriers publish sc.S)
     const int64_t m = S->n;
     const double nu = sqrt(sc.col[1].x);
+    if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 12);
     if (threadIdx.x == 0) {
         // argmin over the shift agents' slices (ascending: ties keep the lowest index)
         AminPart best = kp.amin_part[0];
@@ -266,11 +269,12 @@ static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eage
             kp.lg[6 * m + 5] = sw ? xrecip(fp) : mk(1, 0);
         }
         S->rho_cur = cmul(sc.col[0], cmul(rf, rf));                       // rho_{m+1} / f^2
+        S->n = m + 1;
+        seed_prepare(S);
         S->nu = nu * sqrt(cabs2(rf));
         S->lz_pending = 1;
         S->lz_nu = S->nu;   // current normalisation (matches the rescaled pi buffers)
         S->lz_iter = m + 1;
-        S->n = m + 1;
         S->pending = 0;
         if (!all_retire && m + 1 >= S->itermax) S->status = ST_MAXITER;
         sc.bc[0] = rf;
@@ -287,50 +291,135 @@ static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eage
 }
 
 // ------------------------------------------------------------------------------- seed_step
-// One thread, on a shared copy of the state.  w_raw = <r~|r, q> of the stored vectors.
-static __device__ void seed_step(DevState *S, cplx wraw, int bicg, const KParams &kp) {
-    const cplx sr = S->sr_cur;
-    const cplx w = cmul(cmul(sr, sr), wraw);   // true-scale w_n (shadow scale = conj(sr))
-    const cplx rho = S->rho_cur;
-    const int64_t n = S->n;
-    cplx beta = mk(0, 0), gamma = mk(0, 0);
-    if (n > 0) {
-        beta = xdiv(rho, S->rho_prev);             // EQ-REC-BETA P:L262
-        gamma = xdiv(beta, S->alpha_prev);
-    }
+// Seed scalars of iteration n from the state before the seed step and w_raw = <r~|r, q> of the
+// stored vectors.  Pure: evaluated identically by the update CTAs (deferred mode) and by the
+// commit (seed_step), so both hold bit-identical values.
+static __device__ __forceinline__ bool tiny_abs(cplx v) {   // xabs(v) < 1e-300, cheap path first
+    const double s = fmax(fabs(v.x), fabs(v.y));
+    if (s >= 1e-300) return false;
+    return xabs(v) < 1e-300;
+}
+static __device__ __forceinline__ SeedOut seed_compute(const DevState &S, cplx wraw) {
+    SeedOut o;
+    const cplx sr = S.sr_cur;
+    o.sr = sr;
+    o.w = cmul(cmul(sr, sr), wraw);   // true-scale w_n (shadow scale = conj(sr))
+    const cplx rho = S.rho_cur;
+    const cplx beta = S.beta_nx, gamma = S.gamma_nx;   // EQ-REC-BETA P:L262 (by the finish)
     // EQ-REC-ALPHA-N2: alpha = rho / (<r, A r> - gamma rho), <r, A r> = z_s rho - w
-    const cplx den = csub(csub(cmul(S->zs, rho), w), cmul(gamma, rho));
-    S->w = w;
-    if (xabs(rho) < 1e-300 || xabs(den) < 1e-300) {   // R12
+    const cplx den = csub(csub(cmul(S.zs, rho), o.w), cmul(gamma, rho));
+    o.ok = !(S.rho_small || tiny_abs(den));   // R12
+    o.pad_ = 0;
+    const cplx alpha = o.ok ? xdiv(rho, den) : mk(0, 0);
+    const cplx c = cmul(alpha, gamma);
+    o.alpha = alpha;
+    o.beta = beta;
+    o.c = c;
+    const cplx c1 = cadd(mk(1.0, 0.0), c);
+    o.a_cur = cmul(csub(c1, cmul(alpha, S.zs)), sr);   // EQ-CG-RN-3REC with A r = z_s r - q
+    o.a_q = cmul(alpha, sr);
+    o.a_prev = cmul(mk(-c.x, -c.y), S.sr_prev);
+    return o;
+}
+
+// Next seed step's w-independent parts (beta_{n-1}, gamma, |rho_n| test), from the state after a
+// finish (or the initialisation) — the same operations the seed step itself would do.
+static __device__ __forceinline__ void seed_prepare(DevState *S) {
+    if (S->n > 0) {
+        S->beta_nx = xdiv(S->rho_cur, S->rho_prev);
+        S->gamma_nx = xdiv(S->beta_nx, S->alpha_prev);
+    } else {
+        S->beta_nx = mk(0, 0);
+        S->gamma_nx = mk(0, 0);
+    }
+    S->rho_small = tiny_abs(S->rho_cur);
+}
+
+// Commit evaluated seed scalars to a shared copy of the state (one thread).
+static __device__ void seed_apply(DevState *S, const SeedOut &o, int bicg, const KParams &kp) {
+    const int64_t n = S->n;
+    S->w = o.w;
+    if (!o.ok) {
         S->status = ST_BREAKDOWN;
         return;
     }
-    const cplx alpha = xdiv(rho, den);
-    const cplx c = cmul(alpha, gamma);
-    S->alpha = alpha;
-    S->beta = beta;
-    S->c = c;
-    S->sr_it = sr;
+    S->alpha = o.alpha;
+    S->beta = o.beta;
+    S->c = o.c;
+    S->sr_it = o.sr;
     if (n < kp.lg_cap) {   // coefficient log (recalc)
-        kp.lg[6 * n] = alpha;
-        kp.lg[6 * n + 1] = beta;
-        kp.lg[6 * n + 2] = c;
+        kp.lg[6 * n] = o.alpha;
+        kp.lg[6 * n + 1] = o.beta;
+        kp.lg[6 * n + 2] = o.c;
         kp.lg[6 * n + 3] = S->zs;
         kp.lg[6 * n + 4] = mk(1, 0);
         kp.lg[6 * n + 5] = mk(1, 0);
     }
-    const cplx c1 = cadd(mk(1.0, 0.0), c);
-    S->a_cur = cmul(csub(c1, cmul(alpha, S->zs)), sr);   // EQ-CG-RN-3REC with A r = z_s r - q
-    S->a_q = cmul(alpha, sr);
-    S->a_prev = cmul(mk(-c.x, -c.y), S->sr_prev);
-    S->sr_prev = sr;
+    S->a_cur = o.a_cur;
+    S->a_q = o.a_q;
+    S->a_prev = o.a_prev;
+    S->sr_prev = o.sr;
     S->sr_cur = mk(1.0, 0.0);
-    S->alpha_prev = alpha;
-    S->rho_prev = rho;
+    S->alpha_prev = o.alpha;
+    S->rho_prev = S->rho_cur;
     S->n_started = n + 1;
     S->pending = 1;
     S->bscale[(n + 1) % 3] = mk(1.0, 0.0);   // the shift step writes pi_{n+1} unscaled
     S->nspmv += bicg ? 2 : 1;
+}
+
+// One thread, on a shared copy of the state: evaluate and commit the seed step.
+static __device__ void seed_step(DevState *S, cplx wraw, int bicg, const KParams &kp) {
+    seed_apply(S, seed_compute(*S, wraw), bicg, kp);
+}
+
+// w_raw of the deferred seed step: the partials of the current half reduced in a fixed order
+// that does not depend on the CTA size (threads 0..255 take strided subsequences, then a fixed
+// warp tree, then warps 0..7 in order), so every CTA that evaluates it gets the same bits.  All
+// threads call it (blockDim >= 256); ends with a barrier.
+static __device__ __noinline__ cplx reduce_w_fixed(const cplx *part, int n, cplx *red8) {
+    const int tid = threadIdx.x;
+    cplx v = mk(0.0, 0.0);
+    if (tid < 256) {
+        int i = tid;
+        for (; i + 3 * 256 < n; i += 4 * 256) {
+            const cplx a = ldcg(part + i), b = ldcg(part + i + 256), c = ldcg(part + i + 512),
+                       d = ldcg(part + i + 768);
+            v = cadd(cadd(cadd(cadd(v, a), b), c), d);
+        }
+        for (; i < n; i += 256) v = cadd(v, ldcg(part + i));
+        v = warp_sum(v);
+        if ((tid & 31) == 0) red8[tid >> 5] = v;
+    }
+    __syncthreads();
+    cplx s = red8[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) s = cadd(s, red8[w]);
+    __syncthreads();
+    return s;
+}
+
+// The finish of a pending iteration as the agents run it.  Deferred mode: first commit the seed
+// step of that iteration (the scalars the update CTAs evaluated, recorded in S.rec by CTA 0);
+// a breakdown there ends the run (with the retirement test left pending by the previous finish
+// applied eagerly).  Then finish_step.
+static __device__ void agent_finish(const KParams &kp, StepScratch &sc, bool eager) {
+    if (!kp.defer) {
+        finish_step(kp, sc, eager);
+        return;
+    }
+    state_load_nosync(sc.S, kp.st);
+    __syncthreads();
+    if (threadIdx.x == 0 && sc.S.status == ST_ITERATING) seed_apply(&sc.S, sc.S.rec, kp.bicg, kp);
+    __syncthreads();
+    if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 11);
+    if (sc.S.status == ST_BREAKDOWN) {
+        if (sc.S.lz_pending) retire_pass(kp, sc);
+        if (threadIdx.x == 0) sc.S.pending = 0;
+        state_store(kp.st, sc.S);
+        return;
+    }
+    finish_step(kp, sc, eager, /*loaded=*/true);
 }
 
 // ------------------------------------------------------------------------------- shift recurrences
@@ -368,7 +457,7 @@ struct ShiftScratch {
     int ri[32], rc[32];
     cplx f, fp;
 };
-static __device__ void shift_step(const KParams &kp, ShiftScratch &ss, int agent) {
+static __device__ void shift_step(const KParams &kp, ShiftScratch &ss, int agent, cplx alpha, cplx beta, cplx c) {
     DevState *S = kp.st;
     const int64_t n = S->n;
     const int nzt = kp.nz, nl = kp.nl, NT = blockDim.x, tid = threadIdx.x;
@@ -382,7 +471,7 @@ static __device__ void shift_step(const KParams &kp, ShiftScratch &ss, int agent
     const cplx *zz = kp.z + k_lo;
     uint8_t *actv = kp.active + k_lo;
     const cplx bc = S->bscale[n % 3], bp = S->bscale[(n + 2) % 3];
-    const cplx alpha = S->alpha, beta = S->beta, c = S->c, zs = S->zs;
+    const cplx zs = S->zs;
     const bool lz = S->lz_pending != 0 && S->lz_iter == n;
     const double lz_nu = S->lz_nu, tol = S->tol;
     int cnt = 0, bi = -1;

@@ -50,6 +50,54 @@ __global__ void __launch_bounds__(kThreads) init_kernel(KParams kp, const cplx *
     }
 }
 
+
+// Seed scalars of the iteration this update kernel advances.  Deferred mode (world == 1): every
+// CTA reduces the SpMV's w partials in the fixed order of reduce_w_fixed and evaluates
+// seed_compute itself (thread 0, broadcast through shared memory) — the same bits the next
+// finish will commit; no last-CTA hand-off, no serial tail on the critical path.  Otherwise the
+// seed step already ran (SpMV's last CTA, or seed_kernel after the all-reduce) and the scalars
+// are read from the state.  Returns false on a breakdown (deferred mode; the commit reports it).
+// CTA 0 publishes seq (the SpMV's buffer / partial-half counter) and, deferred, pending.
+struct UpdSeed {
+    DevState S;
+    SeedOut o;
+    int64_t nsx;   // n_started after the seed step of this iteration
+    cplx red8[8];
+};
+static __device__ __forceinline__ bool update_seed(const KParams &kp, UpdSeed &us) {
+    DevState *st = kp.st;
+    if (kp.defer) {
+        const int64_t m = st->n_started;
+        state_load_nosync(us.S, st);   // (published by the barriers of the reduction)
+        const cplx w = reduce_w_fixed(kp.part_w + (m & 1) * kp.wred_stride + kp.wred_off, kp.wred_n, us.red8);
+        if (threadIdx.x == 0) {
+            us.o = seed_compute(us.S, w);
+            us.nsx = m + 1;
+            if (blockIdx.x == 0) {   // (nothing in this kernel reads rec, pending or seq)
+                st->rec = us.o;
+                st->pending = 1;     // the next finish commits rec (or reports the breakdown)
+                if (us.o.ok) st->seq = m + 1;
+            }
+        }
+        __syncthreads();
+        return us.o.ok != 0;
+    }
+    if (threadIdx.x == 0) {
+        us.o.alpha = st->alpha;
+        us.o.beta = st->beta;
+        us.o.c = st->c;
+        us.o.a_cur = st->a_cur;
+        us.o.a_q = st->a_q;
+        us.o.a_prev = st->a_prev;
+        us.o.sr = st->sr_it;
+        us.o.ok = 1;
+        us.nsx = st->n_started;
+        if (blockIdx.x == 0) st->seq = us.nsx;
+    }
+    __syncthreads();
+    return true;
+}
+
 // ============================================================================ fused update
 // Each thread owns R rows per sweep (rows tid, tid+256, ... of a 256*R chunk) and issues all of
 // their loads before any arithmetic, so 4R+ independent 16-byte loads are in flight per thread.
@@ -58,26 +106,53 @@ __global__ void __launch_bounds__(kThreads, FULL ? 2 : 4)
 update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
     extern __shared__ cplx dyn[];  // FULL: coef[3 nz], flags[nz], list[nz]
     __shared__ ShiftScratch ss;
+    __shared__ UpdSeed us;
     pdl_wait();
     DevState *st = kp.st;
     if (st->status != ST_ITERATING) return;
-    if (blockIdx.x < kp.n_agents) {   // shift agents (a4 + a6 + pending a8), beside the streaming CTAs
-        if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 5);
-        shift_step(kp, ss, blockIdx.x);
-        __syncthreads();
-        if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 6);
-        return;
-    }
-    if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 7);
     const int wb = blockIdx.x - kp.n_agents, nwb = gridDim.x - kp.n_agents;
-    const int64_t ns = st->n_started;            // seed step of iteration n ran: ns = n + 1
+    const int64_t ns = st->n_started + (kp.defer ? 1 : 0);   // after the seed step of iteration n
     const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);
     const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);
     cplx *__restrict__ rn_ = pick3(kp.r, ns);
     const cplx *__restrict__ tc_ = pick3(kp.t, ns + 2);
     const cplx *__restrict__ tp_ = pick3(kp.t, ns + 1);
     cplx *__restrict__ tn_ = pick3(kp.t, ns);
-    const cplx a_cur = st->a_cur, a_q = st->a_q, a_prev = st->a_prev;
+    const int64_t M = kp.M;
+    const int nl = kp.nl;
+    const int64_t chunk = (int64_t)kThreads * R;
+    const int64_t base0 = (int64_t)wb * chunk;
+    // streamed rows of a chunk; the first chunk's loads do not depend on the seed scalars and
+    // are issued before them (their latency overlaps the w reduction and the seed step)
+    cplx rc[R], rp[R], qi[R], tc[R], tp[R], qti[R], lv[R][NLMAX];
+    auto load_chunk = [&](int64_t base) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
+            if (i < M) {
+                rc[k] = ldg_cs(rc_ + i);
+                rp[k] = ldg_cs(rp_ + i);
+                qi[k] = ldg_cs(q + i);
+                if (BICG) { tc[k] = ldg_cs(tc_ + i); tp[k] = ldg_cs(tp_ + i); qti[k] = ldg_cs(qt + i); }
+#pragma unroll
+                for (int l = 0; l < NLMAX; ++l)
+                    if (l < nl) lv[k][l] = ldg_cs(kp.left + (int64_t)l * M + i);
+            }
+        }
+    };
+    if (wb >= 0 && base0 < M) load_chunk(base0);
+    if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 13);
+    if (!update_seed(kp, us)) return;
+    if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 14);
+    if (blockIdx.x < kp.n_agents) {   // shift agents (a4 + a6 + pending a8), beside the streaming CTAs
+        if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 5);
+        shift_step(kp, ss, blockIdx.x, us.o.alpha, us.o.beta, us.o.c);
+        __syncthreads();
+        if (blockIdx.x == 0) dbg_stamp(kp.dbg_ts, 6);
+        return;
+    }
+    if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 7);
+    const cplx a_cur = us.o.a_cur, a_q = us.o.a_q, a_prev = us.o.a_prev;
     const cplx ac_cur = cconj(a_cur), ac_q = cconj(a_q), ac_prev = cconj(a_prev);
     int nact = 0;
     cplx *coef = dyn;      // FULL: [3 nz] coefficients, dense by shift index
@@ -95,7 +170,7 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
         const cplx bc = st->bscale[n % 3], bp = st->bscale[(n + 2) % 3];
         const bool lz = st->lz_pending != 0 && st->lz_iter == n;
         const double lz_nu = st->lz_nu, tol = st->tol;
-        const cplx alpha = st->alpha, beta = st->beta, c = st->c, zs = st->zs, sr = st->sr_it;
+        const cplx alpha = us.o.alpha, beta = us.o.beta, c = us.o.c, zs = st->zs, sr = us.o.sr;
         for (int k = threadIdx.x; k < nz; k += blockDim.x) {
             bool on = kp.active[k] != 0;
             const cplx pik = cmul(cur[k], bc), piok = cmul(prv[k], bp);
@@ -140,24 +215,8 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
     cplx acc[2 + NLMAX];
 #pragma unroll
     for (int j = 0; j < 2 + NLMAX; ++j) acc[j] = mk(0.0, 0.0);
-    const int64_t M = kp.M;
-    const int nl = kp.nl;
-    const int64_t chunk = (int64_t)kThreads * R;
-    for (int64_t base = (int64_t)wb * chunk; base < M; base += (int64_t)nwb * chunk) {
-        cplx rc[R], rp[R], qi[R], tc[R], tp[R], qti[R], lv[R][NLMAX];
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
-            if (i < M) {
-                rc[k] = ldg_cs(rc_ + i);
-                rp[k] = ldg_cs(rp_ + i);
-                qi[k] = ldg_cs(q + i);
-                if (BICG) { tc[k] = ldg_cs(tc_ + i); tp[k] = ldg_cs(tp_ + i); qti[k] = ldg_cs(qt + i); }
-#pragma unroll
-                for (int l = 0; l < NLMAX; ++l)
-                    if (l < nl) lv[k][l] = ldg_cs(kp.left + (int64_t)l * M + i);
-            }
-        }
+    for (int64_t base = base0; base < M; base += (int64_t)nwb * chunk) {
+        if (base != base0) load_chunk(base);
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
@@ -247,23 +306,25 @@ update_proj_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restric
     __shared__ cplx rtile[kThreads];
     __shared__ cplx scratch[4 * (kThreads / 32)];
     __shared__ cplx lsum[32][1];
+    __shared__ UpdSeed us;
     pdl_wait();
     DevState *st = kp.st;
     if (st->status != ST_ITERATING) return;
+    if (!update_seed(kp, us)) return;
     if (blockIdx.x < kp.n_agents) {   // shift agents, beside the streaming CTAs
-        shift_step(kp, ss, blockIdx.x);
+        shift_step(kp, ss, blockIdx.x, us.o.alpha, us.o.beta, us.o.c);
         return;
     }
     const int wb = blockIdx.x - kp.n_agents, nwb = gridDim.x - kp.n_agents;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ns = st->n_started;
+    const int64_t ns = us.nsx;
     const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);
     const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);
     cplx *__restrict__ rn_ = pick3(kp.r, ns);
     const cplx *__restrict__ tc_ = pick3(kp.t, ns + 2);
     const cplx *__restrict__ tp_ = pick3(kp.t, ns + 1);
     cplx *__restrict__ tn_ = pick3(kp.t, ns);
-    const cplx a_cur = st->a_cur, a_q = st->a_q, a_prev = st->a_prev;
+    const cplx a_cur = us.o.a_cur, a_q = us.o.a_q, a_prev = us.o.a_prev;
     const cplx ac_cur = cconj(a_cur), ac_q = cconj(a_q), ac_prev = cconj(a_prev);
     const int64_t M = kp.M;
     const int nl = kp.nl;

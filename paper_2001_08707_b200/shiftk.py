@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshiftk.so")
+LIB_PATH = os.environ.get("SHIFTK_LIB") or os.path.join(_HERE, "libshiftk.so")   # (override: experiments)
 
 COCG, BICG = 0, 1
 OP_HEISENBERG, OP_CSR_REAL, OP_CSR_CPLX, OP_RC, OP_HEISENBERG_SZ = 0, 1, 2, 3, 4

@@ -10,7 +10,8 @@ g = make_solver(to_device(p))
 g.run(20)
 names = {0: "spmv_worker1_start", 1: "agent_start", 2: "finish_done", 3: "last_cta", 4: "seed_done",
          5: "shift_agent_start", 6: "shift_done", 7: "upd_worker1_start", 8: "upd_lastcta_end",
-         9: "seed_reduced"}
+         9: "seed_reduced", 10: "commit_reduced", 11: "commit_seeded", 12: "finish_reduced",
+         13: "upd_w0_enter", 14: "upd_w0_seeded"}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if "flush" in sys.argv else None
 for i in range(4):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -22,6 +23,6 @@ for i in range(4):
     torch.cuda.synchronize()
     ts = g.debug_timestamps()
     t0 = ts[0]
-    d = {names[k]: int(ts[k] - t0) for k in range(10)}
+    d = {names[k]: int(ts[k] - t0) for k in range(15)}
     d["event_step_ns"] = int(1e6 * a.elapsed_time(b))
     print(d)
