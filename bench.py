@@ -61,7 +61,7 @@ def bytes_per_row(problem, kernel: str) -> float:
     """Algorithmic bytes per row of one launch."""
     nseq = 2 if problem.method == "bicg" else 1
     if kernel == "spmv":
-        if problem.op["kind"] == "heisenberg":
+        if problem.op["kind"] in ("heisenberg", "heisenberg_sz"):   # generated on the fly
             bh = 0.0
         else:
             nnz_row = problem.op["col"].shape[0] / problem.M

@@ -5,24 +5,55 @@
 // i-th one.  rank(s) = sum over the set bits of s, taken in ascending position p_1 < p_2 < ...,
 // of C(p_m, m) (the states below s, counted by their highest differing bit).
 //
-// One thread per row: unrank i bit by bit from the top (C(p, m) from a per-CTA shared-memory
-// table), diagonal J/4 (L - 2 popc(s XOR rot s)), and for each anti-aligned bond the partner's
-// row from the rank of s itself: moving the m-th set bit between positions j and j+1 changes
-// exactly one term, C(j, m) <-> C(j+1, m), i.e. the rank by +-C(j, m-1).  Only the periodic
-// bond (L-1, 0) renumbers the set bits; its partner is ranked from scratch.  The gathers are
-// the cost: a partner of a low bond lies next to the row (coalesced across the warp), a partner
-// of a high bond C(j, m-1) rows away.
+// One thread per sector row, consecutive rows on consecutive lanes:
+//  * unranking — lane 0 of a warp unranks the warp's first row bit by bit from the top; the
+//    other lanes step from it inside the block of states that share the bits >= 12: there the
+//    12 low bits run through the 12-bit patterns with a fixed popcount in ascending order, a
+//    shared-memory table (lo_list; lo_idx gives a pattern's position).  Only lanes whose row
+//    leaves that block (a few per cent) unrank themselves.
+//  * bonds — the diagonal is J/4 (L - 2 popc(s XOR rot s)); for every anti-aligned open bond
+//    (j, j+1) the partner's row follows from the row's own rank: moving the m-th set bit between
+//    j and j+1 changes one term, C(j, m) <-> C(j+1, m), i.e. the rank by +-C(j, m-1).  Only the
+//    periodic bond (L-1, 0) renumbers the set bits: its partner is ranked from the low-bit table
+//    plus the high set bits.
+//  * 32-bit state arithmetic for L <= 31 (popc/ffs/shifts are single instructions).
+// The gathers r[partner] are the remaining cost: a low bond's partner is a neighbouring row
+// (coalesced over the warp), a high bond's C(j, m-1) rows away (still consecutive across the
+// warp, since the warp's states share their high bits).
+#include <mutex>
+
 #include "kernels.cuh"
 #include "spmv_common.cuh"
 
 namespace sk {
 
 constexpr int kSzMaxL = 34;
+constexpr int kSzLoBits = 12;
+constexpr int kSzLo = 1 << kSzLoBits;
+constexpr int kSzBatch = 8;   // partner gathers in flight per thread
 
-template <int NRHS>
+// host-built tables, copied into every CTA's shared memory
+struct __align__(16) SzTables {
+    unsigned long long C[kSzMaxL + 1][kSzMaxL + 1];   // binomials, zero for k > n
+    uint16_t lo_list[kSzLo];   // 12-bit patterns sorted by (popcount, value)
+    uint16_t lo_idx[kSzLo];    // position of a pattern within its popcount class
+    int32_t lo_off[kSzLoBits + 2];   // start of each popcount class in lo_list
+};
+__device__ SzTables g_sz_tab;
+
+template <typename U>
+static __device__ __forceinline__ int popcU(U v) {
+    return sizeof(U) == 4 ? __popc((unsigned)v) : __popcll((unsigned long long)v);
+}
+template <typename U>
+static __device__ __forceinline__ int ffsU(U v) {
+    return sizeof(U) == 4 ? __ffs((int)v) - 1 : __ffsll((long long)v) - 1;
+}
+
+template <int NRHS, typename U>
 __global__ void __launch_bounds__(kThreads) heisenberg_sz_kernel(SpmvArgs a, KParams kp, int L, int nup, double J) {
     __shared__ StepScratch sc;
-    __shared__ unsigned long long C[kSzMaxL + 1][kSzMaxL + 2];   // C[n][k], zero for k > n
+    __shared__ SzTables tab;
     bool agent;
     int buf;
     if (!spmv_enter(a, agent, buf, sc, kp)) return;
@@ -31,63 +62,95 @@ __global__ void __launch_bounds__(kThreads) heisenberg_sz_kernel(SpmvArgs a, KPa
     const double qJ = 0.25 * J, hJ = 0.5 * J;
     const int64_t M = a.M;
     const int off = a.st ? 1 : 0;
+    const int lane = threadIdx.x & 31;
     cplx w = mk(0.0, 0.0);
     if (!agent) {
-        for (int e = threadIdx.x; e < (kSzMaxL + 1) * (kSzMaxL + 2); e += blockDim.x) {
-            const int n = e / (kSzMaxL + 2), k = e % (kSzMaxL + 2);
-            unsigned long long c = 0;
-            if (k <= n) {   // exact: C(n, j) * (n - k + j) / j stays below 2^40 for n <= 34
-                c = 1;
-                for (int j = 1; j <= k; ++j) c = c * (unsigned long long)(n - k + j) / (unsigned long long)j;
-            }
-            C[n][k] = c;
+        {   // tables -> shared memory
+            const uint4 *src = (const uint4 *)&g_sz_tab;
+            uint4 *dst = (uint4 *)&tab;
+            for (int e = threadIdx.x; e < (int)(sizeof(SzTables) / 16); e += blockDim.x) dst[e] = src[e];
         }
         __syncthreads();
-        for (int64_t i = (int64_t)(blockIdx.x - off) * blockDim.x + threadIdx.x; i < M;
-             i += (int64_t)(gridDim.x - off) * blockDim.x) {
-            // unrank
-            uint64_t s = 0;
-            {
-                uint64_t rank = (uint64_t)i;
-                int m = nup;
-                for (int p = L - 1; p >= 0 && m > 0; --p) {
-                    const uint64_t below = C[p][m];
-                    if (rank >= below) {
-                        s |= 1ull << p;
-                        rank -= below;
-                        --m;
-                    }
+        auto unrank = [&](uint64_t rank) -> U {
+            U s = 0;
+            int m = nup;
+            for (int p = L - 1; p >= 0 && m > 0; --p) {
+                const uint64_t below = tab.C[p][m];
+                if (rank >= below) {
+                    s |= (U)1 << p;
+                    rank -= below;
+                    --m;
                 }
             }
-            const uint64_t x = s ^ ((s >> 1) | ((s & 1ull) << (L - 1)));
-            const double d = qJ * (double)(L - 2 * __popcll(x));
+            return s;
+        };
+        const int64_t stride = (int64_t)(gridDim.x - off) * blockDim.x;
+        for (int64_t i0 = (int64_t)(blockIdx.x - off) * blockDim.x + (threadIdx.x & ~31); i0 < M; i0 += stride) {
+            const int64_t i = i0 + lane;   // this lane's row (the warp's rows are i0 .. i0 + 31)
+            // warp-cooperative unranking
+            U s0 = 0;
+            if (lane == 0) s0 = unrank((uint64_t)i0);
+            s0 = (U)__shfl_sync(0xffffffffu, (unsigned long long)s0, 0);
+            const U hi0 = s0 >> kSzLoBits;
+            const int c = nup - popcU<U>(hi0);
+            const int idx = (int)tab.lo_idx[s0 & (kSzLo - 1)] + lane;
+            if (i >= M) continue;
+            U s;
+            if (c >= 0 && c <= kSzLoBits && idx < (int)tab.C[kSzLoBits][c])
+                s = (hi0 << kSzLoBits) | (U)tab.lo_list[tab.lo_off[c] + idx];
+            else
+                s = unrank((uint64_t)i);
+            const U x = s ^ ((s >> 1) | ((s & (U)1) << (L - 1)));
+            const double d = qJ * (double)(L - 2 * popcU<U>(x));
             const cplx rs = r[i];
             cplx q = mk(d * rs.x, d * rs.y);
             cplx ts = mk(0, 0), qt = mk(0, 0);
             if (NRHS == 2) { ts = t[i]; qt = mk(d * ts.x, d * ts.y); }
-            uint64_t xb = x & ((1ull << (L - 1)) - 1ull);   // open bonds (j, j+1), j < L-1
+            // open bonds (j, j+1), j < L-1: this lane's active ones in batches of kSzBatch, all
+            // of a batch's gathers in flight at once (a data-dependent loop over single bonds
+            // would leave one gather in flight per thread)
+            U xb = x & (((U)1 << (L - 1)) - (U)1);
             while (xb) {
-                const int j = __ffsll((long long)xb) - 1;
-                xb &= xb - 1ull;
-                const int m = __popcll(s & ((2ull << (j + 1)) - 1ull));   // index of the moving bit
-                const int64_t delta = (int64_t)C[j][m - 1];
-                const int64_t pr = ((s >> j) & 1ull) ? i + delta : i - delta;
-                const cplx v = r[pr];
-                q.x = fma(hJ, v.x, q.x);
-                q.y = fma(hJ, v.y, q.y);
-                if (NRHS == 2) {
-                    const cplx vt = t[pr];
-                    qt.x = fma(hJ, vt.x, qt.x);
-                    qt.y = fma(hJ, vt.y, qt.y);
+                int64_t pr[kSzBatch];
+                bool on[kSzBatch];
+#pragma unroll
+                for (int u = 0; u < kSzBatch; ++u) {
+                    on[u] = xb != 0;
+                    pr[u] = i;
+                    if (on[u]) {
+                        const int j = ffsU<U>(xb);
+                        xb &= xb - (U)1;
+                        const int m = popcU<U>(s & (((U)2 << (j + 1)) - (U)1));   // index of the moving bit
+                        const int64_t delta = (int64_t)tab.C[j][m - 1];
+                        pr[u] = ((s >> j) & (U)1) ? i + delta : i - delta;
+                    }
+                }
+                cplx v[kSzBatch], vt[kSzBatch];
+#pragma unroll
+                for (int u = 0; u < kSzBatch; ++u) {
+                    v[u] = on[u] ? r[pr[u]] : mk(0.0, 0.0);
+                    if (NRHS == 2) vt[u] = on[u] ? t[pr[u]] : mk(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < kSzBatch; ++u) {
+                    if (!on[u]) continue;
+                    q.x = fma(hJ, v[u].x, q.x);
+                    q.y = fma(hJ, v[u].y, q.y);
+                    if (NRHS == 2) {
+                        qt.x = fma(hJ, vt[u].x, qt.x);
+                        qt.y = fma(hJ, vt[u].y, qt.y);
+                    }
                 }
             }
-            if ((x >> (L - 1)) & 1ull) {   // periodic bond (L-1, 0): rank the partner afresh
-                uint64_t s2 = s ^ (1ull | (1ull << (L - 1)));
-                int64_t pr = 0;
-                for (int m = 1; s2; ++m) {
-                    const int p = __ffsll((long long)s2) - 1;
-                    s2 &= s2 - 1ull;
-                    pr += (int64_t)C[p][m];
+            if ((x >> (L - 1)) & (U)1) {   // periodic bond (L-1, 0): rank the partner afresh
+                const U s2 = s ^ ((U)1 | ((U)1 << (L - 1)));
+                const U lo = s2 & (U)(kSzLo - 1);
+                int64_t pr = (int64_t)tab.lo_idx[lo];   // sum over the low set bits
+                U h = s2 >> kSzLoBits;
+                for (int m = popcU<U>(lo) + 1; h; ++m) {
+                    const int p = ffsU<U>(h);
+                    h &= h - (U)1;
+                    pr += (int64_t)tab.C[p + kSzLoBits][m];
                 }
                 const cplx v = r[pr];
                 q.x = fma(hJ, v.x, q.x);
@@ -110,11 +173,41 @@ __global__ void __launch_bounds__(kThreads) heisenberg_sz_kernel(SpmvArgs a, KPa
     spmv_exit(a, kp, agent, w, sc);
 }
 
+static cudaError_t sz_tables_init() {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        static SzTables h;
+        for (int n = 0; n <= kSzMaxL; ++n)
+            for (int k = 0; k <= kSzMaxL; ++k)
+                h.C[n][k] = k > n ? 0ull : (k == 0 || k == n ? 1ull : h.C[n - 1][k - 1] + h.C[n - 1][k]);
+        int pos = 0;
+        for (int c = 0; c <= kSzLoBits; ++c) {
+            h.lo_off[c] = pos;
+            int within = 0;
+            for (int v = 0; v < kSzLo; ++v)
+                if (__builtin_popcount((unsigned)v) == c) {
+                    h.lo_list[pos++] = (uint16_t)v;
+                    h.lo_idx[v] = (uint16_t)within++;
+                }
+        }
+        h.lo_off[kSzLoBits + 1] = pos;
+        err = cudaMemcpyToSymbol(g_sz_tab, &h, sizeof(h));
+    });
+    return err;
+}
+
 cudaError_t launch_heisenberg_sz(const SpmvArgs &a, const KParams &kp, int L, int nup, double J, cudaStream_t s) {
+    const cudaError_t e = sz_tables_init();
+    if (e != cudaSuccess) return e;
     const int grid = stream_blocks(a.M) + (a.st ? 1 : 0);
     const bool p = a.st != nullptr;
-    if (a.bicg) return launch_k(heisenberg_sz_kernel<2>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
-    return launch_k(heisenberg_sz_kernel<1>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
+    if (L <= 31) {
+        if (a.bicg) return launch_k(heisenberg_sz_kernel<2, uint32_t>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
+        return launch_k(heisenberg_sz_kernel<1, uint32_t>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
+    }
+    if (a.bicg) return launch_k(heisenberg_sz_kernel<2, uint64_t>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
+    return launch_k(heisenberg_sz_kernel<1, uint64_t>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
 }
 
 }  // namespace sk

@@ -75,7 +75,7 @@ def run_window(problem, n_w, *, full_check=False, flags=0, tol=None):
 
 # ------------------------------------------------------------------------------- operators
 
-@pytest.mark.parametrize("L", [4, 12, 17, 23])
+@pytest.mark.parametrize("L", [4, 12, 17, 23, 24, 25])
 def test_heisenberg_operator_parity(L):
     rng = np.random.default_rng(L)
     r = rng.standard_normal(1 << L) + 1j * rng.standard_normal(1 << L)
