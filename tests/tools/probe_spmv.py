@@ -29,6 +29,17 @@ for L in Ls:
         a.record(); shiftk.apply_operator(op, r, q); b.record(); torch.cuda.synchronize()
         cold.append(1e3 * a.elapsed_time(b))
     cold = sorted(cold)[len(cold) // 2]
+    # cold data, warm code: flush, then the same kernel on another vector, then time on r
+    r2 = torch.randn_like(r)
+    q2 = torch.empty_like(r)
+    colddata = []
+    for i in range(10):
+        flush.fill_(i)
+        shiftk.apply_operator(op, r2, q2)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); shiftk.apply_operator(op, r, q); b.record(); torch.cuda.synchronize()
+        colddata.append(1e3 * a.elapsed_time(b))
+    colddata = sorted(colddata)[len(colddata) // 2]
     # graph of n back-to-back launches (no host overhead)
     st = torch.cuda.Stream()
     gr = torch.cuda.CUDAGraph()
@@ -42,6 +53,6 @@ for L in Ls:
     ev[0].record(); gr.replay(); ev[1].record(); torch.cuda.synchronize()
     graph = 1e3 * ev[0].elapsed_time(ev[1]) / n
     byt = 32 * M
-    out[L] = {"graph_us": round(graph, 2), "graph_GBps": round(byt / graph / 1e3, 1), "warm_us": round(warm, 2), "cold_us": round(cold, 2),
+    out[L] = {"graph_us": round(graph, 2), "graph_GBps": round(byt / graph / 1e3, 1), "warm_us": round(warm, 2), "cold_us": round(cold, 2), "colddata_us": round(colddata, 2),
               "warm_GBps": round(byt / warm / 1e3, 1), "cold_GBps": round(byt / cold / 1e3, 1)}
 print(json.dumps(out, indent=1))
