@@ -17,7 +17,7 @@ int shift_agents(int nz) {
 }
 
 int update_blocks(int64_t M, int nl, int full, int nz) {
-    const int R = full ? 1 : (nl <= 4 ? 2 : 1);   // (the N_left > 4 kernel uses 256-row chunks)
+    const int R = 1;   // rows per thread per chunk (the non-full kernel pipelines two chunks)
     int64_t b = (M + (int64_t)kThreads * R - 1) / ((int64_t)kThreads * R);
     const int64_t cap = 148 * 4 - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
     if (b > cap) b = cap;
@@ -124,23 +124,26 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
     const int64_t base0 = (int64_t)wb * chunk;
     // streamed rows of a chunk; the first chunk's loads do not depend on the seed scalars and
     // are issued before them (their latency overlaps the w reduction and the seed step)
-    cplx rc[R], rp[R], qi[R], tc[R], tp[R], qti[R], lv[R][NLMAX];
-    auto load_chunk = [&](int64_t base) {
+    struct Chunk {
+        cplx rc[R], rp[R], qi[R], tc[R], tp[R], qti[R], lv[R][NLMAX];
+    };
+    Chunk A;
+    auto load_chunk = [&](Chunk &C, int64_t base) {
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
             if (i < M) {
-                rc[k] = ldg_cs(rc_ + i);
-                rp[k] = ldg_cs(rp_ + i);
-                qi[k] = ldg_cs(q + i);
-                if (BICG) { tc[k] = ldg_cs(tc_ + i); tp[k] = ldg_cs(tp_ + i); qti[k] = ldg_cs(qt + i); }
+                C.rc[k] = ldg_cs(rc_ + i);
+                C.rp[k] = ldg_cs(rp_ + i);
+                C.qi[k] = ldg_cs(q + i);
+                if (BICG) { C.tc[k] = ldg_cs(tc_ + i); C.tp[k] = ldg_cs(tp_ + i); C.qti[k] = ldg_cs(qt + i); }
 #pragma unroll
                 for (int l = 0; l < NLMAX; ++l)
-                    if (l < nl) lv[k][l] = ldg_cs(kp.left + (int64_t)l * M + i);
+                    if (l < nl) C.lv[k][l] = ldg_cs(kp.left + (int64_t)l * M + i);
             }
         }
     };
-    if (wb >= 0 && base0 < M) load_chunk(base0);
+    if (wb >= 0 && base0 < M) load_chunk(A, base0);
     if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 13);
     if (!update_seed(kp, us)) return;
     if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 14);
@@ -215,20 +218,19 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
     cplx acc[2 + NLMAX];
 #pragma unroll
     for (int j = 0; j < 2 + NLMAX; ++j) acc[j] = mk(0.0, 0.0);
-    for (int64_t base = base0; base < M; base += (int64_t)nwb * chunk) {
-        if (base != base0) load_chunk(base);
+    auto compute = [&](Chunk &C, int64_t base) {
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const int64_t i = base + threadIdx.x + (int64_t)k * kThreads;
             if (i >= M) continue;
-            cplx rn = cmul(a_cur, rc[k]);
-            rn = cfma(a_q, qi[k], rn);
-            rn = cfma(a_prev, rp[k], rn);
+            cplx rn = cmul(a_cur, C.rc[k]);
+            rn = cfma(a_q, C.qi[k], rn);
+            rn = cfma(a_prev, C.rp[k], rn);
             rn_[i] = rn;
             if (BICG) {
-                cplx tn = cmul(ac_cur, tc[k]);
-                tn = cfma(ac_q, qti[k], tn);
-                tn = cfma(ac_prev, tp[k], tn);
+                cplx tn = cmul(ac_cur, C.tc[k]);
+                tn = cfma(ac_q, C.qti[k], tn);
+                tn = cfma(ac_prev, C.tp[k], tn);
                 tn_[i] = tn;
                 acc[0] = cfma_conj(tn, rn, acc[0]);
             } else {
@@ -237,9 +239,9 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
             acc[1].x = fma(rn.x, rn.x, fma(rn.y, rn.y, acc[1].x));
 #pragma unroll
             for (int l = 0; l < NLMAX; ++l)
-                if (l < nl) acc[2 + l] = cfma_conj(lv[k][l], rn, acc[2 + l]);
+                if (l < nl) acc[2 + l] = cfma_conj(C.lv[k][l], rn, acc[2 + l]);
             if (FULL) {
-                const cplx r0 = rc[k];
+                const cplx r0 = C.rc[k];
                 int j = 0;
                 for (; j + 4 <= nact; j += 4) {
                     cplx pk[4], xk[4];
@@ -269,6 +271,29 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
                     stg_cs(kp.x + off, cfma(coef[3 * kk + 2], pn, xk));
                 }
             }
+        }
+    };
+    const int64_t step = (int64_t)nwb * chunk;
+    if (!FULL) {
+        // software pipeline (two register sets, loop unrolled by two): the next chunk's loads
+        // are in flight while this one is computed
+        Chunk B;
+        int64_t base = base0;
+        while (base < M) {
+            int64_t nb = base + step;
+            if (nb < M) load_chunk(B, nb);
+            compute(A, base);
+            base = nb;
+            if (base >= M) break;
+            nb = base + step;
+            if (nb < M) load_chunk(A, nb);
+            compute(B, base);
+            base = nb;
+        }
+    } else {
+        for (int64_t base = base0; base < M; base += step) {
+            if (base != base0) load_chunk(A, base);
+            compute(A, base);
         }
     }
     __shared__ cplx scratch[(2 + NLMAX) * (kThreads / 32)];
@@ -399,7 +424,7 @@ update_proj_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restric
 
 template <int NLMAX, bool BICG, bool FULL>
 static cudaError_t launch_update_t(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
-    constexpr int R = FULL ? 1 : (NLMAX <= 4 ? 2 : 1);   // must match update_blocks()
+    constexpr int R = 1;   // must match update_blocks()
     const size_t shm = FULL ? (size_t)kp.nz * (3 * sizeof(cplx) + 2 * sizeof(int)) : 0;
     if (FULL && shm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(update_kernel<NLMAX, BICG, FULL, R>,
