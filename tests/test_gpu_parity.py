@@ -194,6 +194,17 @@ def test_c5_scaled_trajectory():
     run_window(p, 20)
 
 
+@pytest.mark.parametrize("name,kw", [("c2", dict(L=14, nz=32)), ("c2", dict(L=11, nz=16)),
+                                     ("c5sz", dict(L=14, nz=32)), ("c2", dict(L=23, nz=8))])
+def test_bicg_on_the_real_chain(name, kw):
+    """BiCG on a real-symmetric operator (allowed; equals COCG in exact arithmetic, Table 1):
+    exercises the two-right-hand-side paths of the tiled (L=14), simple (L=11), sector and
+    (L=23, NRHS=2 falls back to the tiled kernel) Heisenberg SpMV kernels."""
+    import dataclasses
+    p = dataclasses.replace(synth.make_problem(name, **kw), method="bicg")
+    run_window(p, 4 if kw.get("L", 0) >= 20 else 15)
+
+
 # ------------------------------------------------------------------------------- semantics
 
 def test_run_equals_stepwise_bitwise():
