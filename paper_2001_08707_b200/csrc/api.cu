@@ -98,8 +98,9 @@ struct sk_ctx {
     cplx *b = nullptr;            // device copy of b
     cplx *left_owned = nullptr;
     std::vector<void *> allocs;
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph = nullptr;    // `graph_iters` iterations (sk_run chunks)
     int graph_iters = 0;
+    cudaGraphExec_t graph1 = nullptr;   // one iteration (the remainders, single sk_enqueue steps)
     int64_t host_started = 0;     // iterations enqueued (host view, for RC pointers)
     bool pending_host = false;    // an update ran whose finish phase is not yet enqueued
     // tracing
@@ -149,6 +150,7 @@ static void destroy(sk_ctx *c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->graph1) cudaGraphExecDestroy(c->graph1);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (void *p : c->peer_bases)
         if (p) cudaIpcCloseMemHandle(p);
@@ -800,10 +802,12 @@ int sk_get_seed_vectors(sk_ctx *c, const sk_cplx **r, const sk_cplx **rt) {
 }
 
 static int capture_graph(sk_ctx *c, int iters) {
-    if (c->graph && c->graph_iters == iters) return SK_OK;
-    if (c->graph) {
-        cudaGraphExecDestroy(c->graph);
-        c->graph = nullptr;
+    cudaGraphExec_t &slot = iters == 1 ? c->graph1 : c->graph;
+    if (iters == 1 && c->graph1) return SK_OK;
+    if (iters != 1 && c->graph && c->graph_iters == iters) return SK_OK;
+    if (slot) {
+        cudaGraphExecDestroy(slot);
+        slot = nullptr;
     }
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -818,10 +822,10 @@ static int capture_graph(sk_ctx *c, int iters) {
     c->pending_host = ph;
     if (rc != SK_OK) return rc;
     CK(e);
-    e = cudaGraphInstantiate(&c->graph, g, 0);
+    e = cudaGraphInstantiate(&slot, g, 0);
     cudaGraphDestroy(g);
     CK(e);
-    c->graph_iters = iters;
+    if (iters != 1) c->graph_iters = iters;
     return SK_OK;
 }
 
@@ -832,12 +836,22 @@ static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk) {
     if (iters >= chunk && chunk > 1) {
         if ((rc = capture_graph(c, chunk)) != SK_OK) return rc;
     }
+    const int kpi = c->world > 1 ? 3 : 2;   // kernels per iteration (+ the seed kernel)
     while (iters >= chunk && chunk > 1) {
         CK(cudaGraphLaunch(c->graph, c->stream));
-        c->launches += 3 * chunk;
+        c->launches += kpi * chunk;
         c->host_started += chunk;
         c->pending_host = true;
         iters -= chunk;
+    }
+    if (iters > 0 && !c->profiling && c->world == 1) {   // single iterations: a one-iteration graph
+        if ((rc = capture_graph(c, 1)) != SK_OK) return rc;
+        for (; iters > 0; --iters) {
+            CK(cudaGraphLaunch(c->graph1, c->stream));
+            c->launches += kpi;
+            c->host_started += 1;
+            c->pending_host = true;
+        }
     }
     while (iters-- > 0)
         if ((rc = enqueue_iteration(c, nullptr, nullptr)) != SK_OK) return rc;
