@@ -235,6 +235,20 @@ def test_grouped_partials_window_and_determinism():
     assert g.coefficients() == h.coefficients()
 
 
+def test_many_shifts_beyond_the_shared_memory_flags():
+    """N_z = 5000 > 4096: the finish compacts the active flags from global memory and the update
+    uses eight shift agents."""
+    p = synth.make_problem("c2", L=10, nz=5000)
+    run_window(p, 12)
+
+
+def test_full_mode_with_several_left_vectors():
+    """Full x together with N_left = 6 projections (the FULL update kernel with NLMAX = 8)."""
+    import dataclasses
+    p = dataclasses.replace(synth.make_problem("c4", W=12, nz=8, n_left=6), full_x=True)
+    run_window(p, 12, full_check=True)
+
+
 def test_rc_equals_builtin_operator():
     """Reverse communication: caller-computed q = H r gives the same iterates."""
     p = synth.make_problem("c2", L=10, nz=16)
