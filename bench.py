@@ -168,9 +168,24 @@ def run_reference(args, problem):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "config": config_dict(problem, 1),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def host_info():
+    """CPU model and core count of the box the oracle baseline ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count()}
 
 
 def config_dict(problem, world):
@@ -250,9 +265,16 @@ def main():
         return float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
 
     # pass 1 (the value): no instrumentation between the kernels
+    n0 = solver.coefficients()["iterations"]
     with ClockSampler(local) as clk:
         total_ms = timed_pass()
     launches = solver.profile()["launches"] - launches0
+    # active shift-iterations of the timed window: shift k is updated in
+    # iteration m while m < retired_at[k]
+    n1 = solver.coefficients()["iterations"]
+    _, _, ret = solver.shift_state()
+    stop = np.where(ret >= 0, np.minimum(ret, n1), n1)
+    active_its = int(np.clip(stop - n0, 0, None).sum())
     # pass 2 (the kernel shares): the same K steps with CUDA events around each kernel on the
     # solver's stream (the events cost the programmatic launch overlap, so not the value)
     solver.profile_enable(True)
@@ -294,6 +316,8 @@ def main():
                                (("spmv", prof["ms_spmv"]), ("scalar", prof["ms_scalar"]),
                                 ("update", prof["ms_update"]))},
         "iteration_gbs_model": iter_bytes / (total_ms / args.steps * 1e-3) / 1e9,
+        "iteration_gbs_model_frac": iter_bytes / (total_ms / args.steps * 1e-3) / 1e9 / peak,
+        "active_shift_iterations_per_s": active_its / (total_ms * 1e-3),
         "gpu_launches": launches,
         "solver_state": {"iterations": coeffs["iterations"], "n_active": coeffs["n_active"],
                          "switches": coeffs["switches"]},
@@ -333,6 +357,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         its, dt = oracle_sample(problem, args.cpu_budget, 400)
         line["cpu_baseline"] = {"value": problem.n_shift * its / dt, "unit": UNIT, "cores": 1,
+                                "host": host_info(),
                                 "kind": "oracle",
                                 "sample": f"first {its} iterations of {problem.name} (full size), "
                                           f"{dt:.1f} s single-threaded"}
