@@ -381,13 +381,14 @@ static __device__ __noinline__ cplx reduce_w_fixed(const cplx *part, int n, cplx
     const int tid = threadIdx.x;
     cplx v = mk(0.0, 0.0);
     if (tid < 256) {
-        int i = tid;
-        for (; i + 3 * 256 < n; i += 4 * 256) {
-            const cplx a = ldcg(part + i), b = ldcg(part + i + 256), c = ldcg(part + i + 512),
-                       d = ldcg(part + i + 768);
+        for (int i = tid; i < n; i += 4 * 256) {   // four loads in flight, predicated at the end
+            const cplx z = mk(0.0, 0.0);
+            const cplx a = ldcg(part + i);
+            const cplx b = i + 256 < n ? ldcg(part + i + 256) : z;
+            const cplx c = i + 512 < n ? ldcg(part + i + 512) : z;
+            const cplx d = i + 768 < n ? ldcg(part + i + 768) : z;
             v = cadd(cadd(cadd(cadd(v, a), b), c), d);
         }
-        for (; i < n; i += 256) v = cadd(v, ldcg(part + i));
         v = warp_sum(v);
         if ((tid & 31) == 0) red8[tid >> 5] = v;
     }
