@@ -43,13 +43,17 @@ static __device__ __forceinline__ bool spmv_enter(const SpmvArgs &a, bool &agent
     buf = 0;
     pdl_wait();
     if (!a.st) return true;
-    if (a.st->status != ST_ITERATING) return false;
-    buf = (int)(a.st->seq % 3);   // (seq is written only by the update kernel)
+    // the three words read together (one round trip; seq is written only by the update kernel)
+    const int32_t status = a.st->status;
+    const int64_t seq = a.st->seq;
+    const int32_t pending = a.st->pending;
+    if (status != ST_ITERATING) return false;
+    buf = (int)(seq % 3);
     if (blockIdx.x == 1) dbg_stamp(kp.dbg_ts, 0);                 // first worker CTA starts
     if (blockIdx.x == 0) {
         agent = true;
         dbg_stamp(kp.dbg_ts, 1);
-        if (a.st->pending) agent_finish(kp, sc, /*eager=*/false);
+        if (pending) agent_finish(kp, sc, /*eager=*/false);
         dbg_stamp(kp.dbg_ts, 2);                                   // finish agent done
     }
     return true;
