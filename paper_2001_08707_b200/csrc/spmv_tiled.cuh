@@ -119,24 +119,59 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
             }
         }
         __syncthreads();   // tile staged
+        // Bonds (i, i+1), i < T-1, inside the tile.  The tile's low bits of state ls = tid + 256 k
+        // are tid (bits 0..7) and k (bits 8, 9), so: bonds i <= 6 are decided by tid alone (one
+        // test per thread, the four states' partners at tid ^ (3 << i) + 256 k: constant
+        // offsets); bond 7 by tid bit 7 and k bit 0 (partner k ^ 1); bond 8 by k alone — a
+        // compile-time choice between the thread's own states.
+        static_assert(T == 10 && kThreads == 256 && PER == 4, "bit split assumes 1024-state tiles");
+        {
+            const unsigned xt = (unsigned)(tid ^ (tid >> 1));
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int ls = tid + k * kThreads;
-            const U s = base + (U)ls;
-            const U x = s ^ (s >> 1);   // bit i (< T-1): sites i, i+1 anti-aligned
+            for (int i = 0; i < 7; ++i) {
+                if ((xt >> i) & 1u) {
+                    const int lp = tid ^ (3 << i);
 #pragma unroll
-            for (int i = 0; i < T - 1; ++i) {
-                if ((x >> i) & (U)1) {
-                    const cplx v = tile[ls ^ (3 << i)];
+                    for (int k = 0; k < PER; ++k) {
+                        const cplx v = tile[lp + k * kThreads];
+                        q[k].x = fma(hJ, v.x, q[k].x);
+                        q[k].y = fma(hJ, v.y, q[k].y);
+                        if (NRHS == 2) {
+                            const cplx vt = tile[TS + lp + k * kThreads];
+                            qt[k].x = fma(hJ, vt.x, qt[k].x);
+                            qt[k].y = fma(hJ, vt.y, qt[k].y);
+                        }
+                    }
+                }
+            }
+            const int b7 = (tid >> 7) & 1, lp7 = tid ^ 128;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                if (b7 ^ (k & 1)) {   // bond (7, 8)
+                    const cplx v = tile[lp7 + (k ^ 1) * kThreads];
                     q[k].x = fma(hJ, v.x, q[k].x);
                     q[k].y = fma(hJ, v.y, q[k].y);
                     if (NRHS == 2) {
-                        const cplx vt = tile[TS + (ls ^ (3 << i))];
+                        const cplx vt = tile[TS + lp7 + (k ^ 1) * kThreads];
+                        qt[k].x = fma(hJ, vt.x, qt[k].x);
+                        qt[k].y = fma(hJ, vt.y, qt[k].y);
+                    }
+                }
+                if ((k ^ (k >> 1)) & 1) {   // bond (8, 9): k = 1, 2, partner k ^ 3
+                    const cplx v = tile[tid + (k ^ 3) * kThreads];
+                    q[k].x = fma(hJ, v.x, q[k].x);
+                    q[k].y = fma(hJ, v.y, q[k].y);
+                    if (NRHS == 2) {
+                        const cplx vt = tile[TS + tid + (k ^ 3) * kThreads];
                         qt[k].x = fma(hJ, vt.x, qt[k].x);
                         qt[k].y = fma(hJ, vt.y, qt[k].y);
                     }
                 }
             }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int ls = tid + k * kThreads;
             a.q[lbase + ls] = q[k];
             if (NRHS == 2) {
                 a.qt[lbase + ls] = qt[k];
