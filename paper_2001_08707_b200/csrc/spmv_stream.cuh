@@ -201,16 +201,34 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
                     if (lane == 0) mb_arrive(&ring_empty[s]);
                     ++it;
                 }
-                // bonds (i, i+1), i < T-1, inside the tile
+                // bonds (i, i+1), i < T-1, inside the tile, split by bit position as in the
+                // tiled kernel: bonds 0..6 by the consumer index alone (constant-offset
+                // partners), bond 7 by its bit 7 and e bit 0, bond 8 by e alone
+                static_assert(T == 10 && kStreamConsumers == 256 && PER == 4, "bit split assumes 1024-state tiles");
+                {
+                    const unsigned xt = (unsigned)(tid ^ (tid >> 1));
 #pragma unroll
-                for (int e = 0; e < PER; ++e) {
-                    const int ls = tid + e * kStreamConsumers;
-                    const U s = base + (U)ls;
-                    const U x = s ^ (s >> 1);
+                    for (int i = 0; i < 7; ++i) {
+                        if ((xt >> i) & 1u) {
+                            const int lp = tid ^ (3 << i);
 #pragma unroll
-                    for (int i = 0; i < T - 1; ++i) {
-                        if ((x >> i) & (U)1) {
-                            const cplx v = ot[ls ^ (3 << i)];
+                            for (int e = 0; e < PER; ++e) {
+                                const cplx v = ot[lp + e * kStreamConsumers];
+                                q[e].x = fma(hJ, v.x, q[e].x);
+                                q[e].y = fma(hJ, v.y, q[e].y);
+                            }
+                        }
+                    }
+                    const int b7 = (tid >> 7) & 1, lp7 = tid ^ 128;
+#pragma unroll
+                    for (int e = 0; e < PER; ++e) {
+                        if (b7 ^ (e & 1)) {   // bond (7, 8)
+                            const cplx v = ot[lp7 + (e ^ 1) * kStreamConsumers];
+                            q[e].x = fma(hJ, v.x, q[e].x);
+                            q[e].y = fma(hJ, v.y, q[e].y);
+                        }
+                        if ((e ^ (e >> 1)) & 1) {   // bond (8, 9): partner e ^ 3 (own registers)
+                            const cplx v = v0[e ^ 3];
                             q[e].x = fma(hJ, v.x, q[e].x);
                             q[e].y = fma(hJ, v.y, q[e].y);
                         }
