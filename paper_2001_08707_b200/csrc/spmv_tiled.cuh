@@ -85,7 +85,36 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
         if (L - 1 > T) {
             const U tbits = base >> T;   // bit (i - T) of tbits = site i, for i >= T
             U act = (tbits ^ (tbits >> 1)) & ((((U)1) << (L - 1 - T)) - (U)1);   // bonds T..L-2
-            while (act) {
+            // full rounds of NB partner tiles without predication (the active set is uniform per
+            // tile), then at most one predicated round for the remainder
+            while (((L <= 31) ? __popc((unsigned)act) : __popcll((unsigned long long)act)) >= NB) {
+                const cplx *pt[NB], *ptt[NB];
+#pragma unroll
+                for (int m = 0; m < NB; ++m) {
+                    const int pos = (L <= 31) ? __ffs((int)act) - 1 : __ffsll((long long)act) - 1;
+                    act &= act - (U)1;
+                    const U pb = base ^ ((U)3 << (pos + T));
+                    pt[m] = rv.at(pb) + tid;
+                    ptt[m] = NRHS == 2 ? tv.at(pb) + tid : nullptr;
+                }
+                cplx v[NB][PER], vt[NB][NRHS == 2 ? PER : 1];
+#pragma unroll
+                for (int m = 0; m < NB; ++m)
+#pragma unroll
+                    for (int k = 0; k < PER; ++k) {
+                        v[m][k] = pt[m][k * kThreads];
+                        if (NRHS == 2) vt[m][k] = ptt[m][k * kThreads];
+                    }
+#pragma unroll
+                for (int m = 0; m < NB; ++m)
+#pragma unroll
+                    for (int k = 0; k < PER; ++k) {
+                        q[k].x = fma(hJ, v[m][k].x, q[k].x);
+                        q[k].y = fma(hJ, v[m][k].y, q[k].y);
+                        if (NRHS == 2) { qt[k].x = fma(hJ, vt[m][k].x, qt[k].x); qt[k].y = fma(hJ, vt[m][k].y, qt[k].y); }
+                    }
+            }
+            if (act) {
                 int bi[NB];
 #pragma unroll
                 for (int m = 0; m < NB; ++m) {
