@@ -143,7 +143,10 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
             }
         }
     };
+    Chunk B;   // (non-full: the second chunk is also loaded before the seed scalars)
+    const int64_t step = (int64_t)nwb * chunk;
     if (wb >= 0 && base0 < M) load_chunk(A, base0);
+    if (!FULL && wb >= 0 && base0 + step < M) load_chunk(B, base0 + step);
     if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 13);
     if (!update_seed(kp, us)) return;
     if (blockIdx.x == kp.n_agents) dbg_stamp(kp.dbg_ts, 14);
@@ -273,22 +276,18 @@ update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ q
             }
         }
     };
-    const int64_t step = (int64_t)nwb * chunk;
     if (!FULL) {
-        // software pipeline (two register sets, loop unrolled by two): the next chunk's loads
-        // are in flight while this one is computed
-        Chunk B;
+        // software pipeline (two register sets, loop unrolled by two): A holds the chunk at
+        // `base`, B the next one; a set is refilled with the chunk after next once computed
         int64_t base = base0;
         while (base < M) {
-            int64_t nb = base + step;
-            if (nb < M) load_chunk(B, nb);
             compute(A, base);
-            base = nb;
+            if (base + 2 * step < M) load_chunk(A, base + 2 * step);
+            base += step;
             if (base >= M) break;
-            nb = base + step;
-            if (nb < M) load_chunk(A, nb);
             compute(B, base);
-            base = nb;
+            if (base + 2 * step < M) load_chunk(B, base + 2 * step);
+            base += step;
         }
     } else {
         for (int64_t base = base0; base < M; base += step) {
