@@ -830,7 +830,10 @@ static int capture_graph(sk_ctx *c, int iters) {
 }
 
 // Enqueue `iters` iterations: full graph chunks, then single iterations.
-static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk) {
+// single1: iterations left over below a chunk go through a cached one-iteration graph (the
+// repeated single-step sk_enqueue of a timing loop) instead of direct launches (sk_run, whose
+// remainders are rare and should not pay a second capture).
+static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk, bool single1 = false) {
     int rc;
     if (c->profiling) chunk = 1;   // individual launches bracketed by events
     if (iters >= chunk && chunk > 1) {
@@ -844,7 +847,7 @@ static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk) {
         c->pending_host = true;
         iters -= chunk;
     }
-    if (iters > 0 && !c->profiling && c->world == 1) {   // single iterations: a one-iteration graph
+    if (single1 && iters > 0 && !c->profiling && c->world == 1) {   // a one-iteration graph
         if ((rc = capture_graph(c, 1)) != SK_OK) return rc;
         for (; iters > 0; --iters) {
             CK(cudaGraphLaunch(c->graph1, c->stream));
@@ -885,7 +888,7 @@ int sk_enqueue(sk_ctx *c, int64_t iters) {
     if (c->op.kind == SK_OP_RC) return fail(SK_ESTATE, "SK_OP_RC context: use sk_update_rc");
     if (iters < 0) return fail(SK_EINVAL, "iters < 0");
     CK(cudaSetDevice(c->device));
-    return enqueue_iters(c, iters, 16);
+    return enqueue_iters(c, iters, 16, /*single1=*/true);
 }
 
 int sk_get_residual(sk_ctx *c, double *res) {
