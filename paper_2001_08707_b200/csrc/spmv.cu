@@ -54,6 +54,17 @@ bool heis_stream(int L, int64_t M, int bicg) {
     return en == 1 || (M >> kTileBits) >= 8192;
 }
 
+// Tile pairs across the top spin bit (spmv_stream.cuh heisenberg_pair_kernel) on one GPU from
+// L = 24, where the periodic partner would otherwise come from DRAM; SHIFTK_HEIS_PAIRS=0/1.
+bool heis_pairs(int L, int64_t M) {
+    static int en = -1;
+    if (en < 0) {
+        const char *e = getenv("SHIFTK_HEIS_PAIRS");
+        en = (e && e[0] == '0') ? 0 : 1;
+    }
+    return en && L >= 24 && M == (int64_t(1) << L);
+}
+
 int heisenberg_blocks(int L, int64_t M, int bicg) {
     if (heis_stream(L, M, bicg)) {   // two CTAs per SM, one slot left for the finish agent
         const int64_t ntiles = M >> kTileBits, slots = 2 * (int64_t)sm_count() - 1;

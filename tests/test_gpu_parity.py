@@ -235,6 +235,18 @@ def test_grouped_partials_window_and_determinism():
     assert g.coefficients() == h.coefficients()
 
 
+def test_tile_pairs_window_and_determinism():
+    """L=24: the streaming SpMV works on tile pairs across the top spin bit (each the other's
+    periodic partner); oracle window and bit-identical reruns."""
+    p = synth.make_problem("c2", L=24, nz=8)
+    g, o, _, _ = run_window(p, 3)
+    h = make_solver(to_device(p))
+    for _ in range(3):
+        h.update()
+    assert np.array_equal(g.residuals(), h.residuals())
+    assert g.coefficients() == h.coefficients()
+
+
 def test_many_shifts_beyond_the_shared_memory_flags():
     """N_z = 5000 > 4096: the finish compacts the active flags from global memory and the update
     uses eight shift agents."""
