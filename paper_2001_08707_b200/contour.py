@@ -24,19 +24,22 @@ def contour_points(n_z: int, gamma: float, rho: float) -> np.ndarray:
 
 def ss_eigenvalues(op: dict, phis: np.ndarray, gamma: float, rho: float, n_z: int, n_k: int, *,
                    sv_tol: float = 1e-3, tol: float = 1e-10, itermax: int = 20000,
-                   device: str = "cuda:0", return_details: bool = False):
-    """Eigenvalues of H inside |z - gamma| < rho (ascending) from n_l = len(phis) sources."""
+                   device: str = "cuda:0", dev_arrays=None, return_details: bool = False):
+    """Eigenvalues of H inside |z - gamma| < rho (ascending) from n_l = len(phis) sources.
+    CSR operators need their device arrays (`dev_arrays`); a complex Hermitian H is solved
+    with BiCG, a real-symmetric one with COCG (Table 1)."""
     import torch
     dev = torch.device(device)
     n_l, M = phis.shape
     z = contour_points(n_z, gamma, rho)
-    hop = shiftk.make_operator(op, M)
+    hop = shiftk.make_operator(op, M, dev_arrays)
+    method = "bicg" if op["kind"] == "csr_cplx" else "cocg"
     S = torch.empty((n_l * n_k, M), dtype=torch.complex128, device=dev)
     iters = []
     for l in range(n_l):
         nrm = float(np.sqrt(np.vdot(phis[l], phis[l]).real))
         b = torch.from_numpy(np.ascontiguousarray(phis[l] / nrm)).to(dev)
-        sol = shiftk.Solver(hop, "cocg", b, z, full_x=True, tol=tol, itermax=itermax)
+        sol = shiftk.Solver(hop, method, b, z, full_x=True, tol=tol, itermax=itermax)
         st = sol.run(itermax)
         if st != shiftk.CONVERGED:
             raise RuntimeError(f"contour solve {l}: status {st}")

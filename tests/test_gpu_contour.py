@@ -59,3 +59,28 @@ def test_ss_pipeline_reproduces_table3(col, n_l):
     k = min(info["rank"] + 1, sig_o.size)
     assert np.allclose(info["singular_values"][:info["rank"]], sig_o[:info["rank"]], rtol=1e-7)
     assert np.all(info["singular_values"][info["rank"]:k] < 1e-3)
+
+
+def test_ss_on_the_complex_lattice_matches_dense_eigenvalues():
+    """The contour-integral path on a complex Hermitian CSR operator (BiCG, Table 1): the C4
+    Peierls lattice at 8 x 8 sites, eigenvalues inside a circle against a dense eigensolve."""
+    p = synth.make_problem("c4", W=8, nz=4, n_left=1)
+    M = p.M
+    H = np.zeros((M, M), dtype=np.complex128)
+    e = np.zeros(M, dtype=np.complex128)
+    for j in range(M):
+        e[:] = 0
+        e[j] = 1
+        H[:, j] = oracle.apply_op(p.op, e)
+    lam = np.linalg.eigvalsh(H)
+    gaps = np.diff(lam)
+    k = int(np.argmax(gaps[M // 2:M // 2 + 20])) + M // 2   # a well separated window edge
+    gamma = 0.5 * (lam[k - 5] + lam[k])
+    rho = 0.5 * (lam[k] - lam[k - 5]) + 0.5 * gaps[k]
+    want = lam[np.abs(lam - gamma) < rho]
+    rng = np.random.Generator(np.random.PCG64(11))
+    phis = rng.standard_normal((6, M)) + 1j * rng.standard_normal((6, M))
+    arrays = {kk: torch.from_numpy(p.op[kk]).cuda() for kk in ("row_ptr", "col", "val")}
+    ev = contour.ss_eigenvalues(p.op, phis, gamma, rho, 128, 8, dev_arrays=arrays, sv_tol=1e-6)
+    assert ev.size == want.size
+    assert np.max(np.abs(ev - want)) < 1e-7
