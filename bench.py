@@ -244,7 +244,6 @@ def main():
     with torch.cuda.stream(stream):
         solver.enqueue(args.warmup)
     torch.cuda.synchronize()
-    launches0 = solver.profile()["launches"]
 
     def timed_pass(clk=None):
         """K steps, L2 flushed before each (outside the events); returns the summed step ms."""
@@ -265,7 +264,8 @@ def main():
         return float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
 
     # pass 1 (the value): no instrumentation between the kernels
-    n0 = solver.coefficients()["iterations"]
+    n0 = solver.coefficients()["iterations"]   # (may launch the pending finish: before the count)
+    launches0 = solver.profile()["launches"]
     with ClockSampler(local) as clk:
         total_ms = timed_pass()
     launches = solver.profile()["launches"] - launches0
