@@ -261,6 +261,24 @@ def test_full_mode_with_several_left_vectors():
     run_window(p, 12, full_check=True)
 
 
+def test_run_past_convergence_equals_stepwise():
+    """sk_run polls every 64 iterations, so it launches iterations past convergence; they must be
+    no-ops: the same iteration count, residuals and projections as stepping until converged."""
+    p = synth.make_problem("c1", L=10, nz=8)
+    dp = to_device(p)
+    a = make_solver(dp)
+    n = 0
+    while a.update() == shiftk.ITERATING:
+        n += 1
+    b = make_solver(dp)
+    assert b.run(p.itermax, poll_every=64) == shiftk.CONVERGED
+    assert a.coefficients() == b.coefficients()
+    assert np.array_equal(a.residuals(), b.residuals())
+    assert np.array_equal(a.projections(), b.projections())
+    for k in (0, p.n_shift - 1):
+        assert np.array_equal(a.solution(k), b.solution(k))
+
+
 def test_rc_equals_builtin_operator():
     """Reverse communication: caller-computed q = H r gives the same iterates."""
     p = synth.make_problem("c2", L=10, nz=16)
