@@ -217,6 +217,8 @@ int sk_copy_solution(sk_ctx *ctx, int64_t k, sk_cplx *dst, int32_t dst_mem);
    Any pointer may be NULL. */
 int sk_get_shift_state(sk_ctx *ctx, sk_cplx *pi, uint8_t *active, int64_t *retired_at);
 
+/* The current seed and its scalars (sk_coeffs above; the paper's TriDiagComp.dat quantities,
+   P:L638) after finishing any pending iteration.  out: HOST. */
 int sk_get_coefficients(sk_ctx *ctx, sk_coeffs *out);
 
 /* Release everything and set *ctx = NULL.  A second call on NULL returns SK_ESTATE. */
