@@ -84,3 +84,31 @@ def test_unconnected_context_refuses_to_iterate():
     with pytest.raises(shiftk.ShiftkError) as e:
         solver.update()
     assert e.value.code == -5
+
+
+def test_loopback_group_with_the_streaming_kernel():
+    """The multi-rank (MULTI) instantiation of the streaming Heisenberg SpMV — shard-table
+    partner addresses fed to the bulk copies — forced at a small size in a subprocess
+    (SHIFTK_HEIS_STREAM is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, synth, oracle\n"
+        "from test_gpu_multirank import make_group, REL, proj_err\n"
+        "p = synth.make_problem('c5', L=16, nz=32)\n"
+        "g, keep = make_group(p, 4)\n"
+        "o = oracle.Oracle(p.method, p.b, p.z, left=p.left, full_x=p.full_x, tol=p.tol, itermax=p.itermax)\n"
+        "for n in range(12):\n"
+        "    assert g.update() == o.step(p.op)\n"
+        "    ro = o.residuals()\n"
+        "    for m in g.members:\n"
+        "        assert np.all(np.abs(m.residuals() - ro) <= REL * ro), n\n"
+        "        assert np.all(proj_err(m.projections(), o.projections()) <= REL), n\n"
+        "g.close()\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SHIFTK_HEIS_STREAM="1", PYTHONPATH=root + os.pathsep + os.path.join(root, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
