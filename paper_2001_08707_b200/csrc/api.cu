@@ -381,8 +381,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
     kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M, kp.bicg)
-                   : ((H->kind == SK_OP_RC || H->kind == SK_OP_HEISENBERG_SZ) ? sk::stream_blocks(M)
-                                                                              : sk::csr_blocks(M));
+                   : H->kind == SK_OP_HEISENBERG_SZ ? sk::sz_blocks(H->L, M, kp.bicg)
+                   : H->kind == SK_OP_RC ? sk::stream_blocks(M) : sk::csr_blocks(M);
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;

@@ -20,6 +20,7 @@
 // The gathers r[partner] are the remaining cost: a low bond's partner is a neighbouring row
 // (coalesced over the warp), a high bond's C(j, m-1) rows away (still consecutive across the
 // warp, since the warp's states share their high bits).
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -30,6 +31,12 @@ namespace sk {
 constexpr int kSzMaxL = 34;
 constexpr int kSzLoBits = 12;
 constexpr int kSzLo = 1 << kSzLoBits;
+#ifndef SZB_MINB
+#define SZB_MINB 4
+#endif
+#ifndef SZB_BATCH
+#define SZB_BATCH 7
+#endif
 constexpr int kSzBatch = 8;   // partner gathers in flight per thread
 
 // host-built tables, copied into every CTA's shared memory
@@ -173,6 +180,163 @@ __global__ void __launch_bounds__(kThreads) heisenberg_sz_kernel(SpmvArgs a, KPa
     spmv_exit(a, kp, agent, w, sc);
 }
 
+// Block-structured variant (the default from L = 2).  Split a state s into its high part H
+// (bits kb .. L-1, kb = min(12, L-1)) and its low pattern lo (bits 0 .. kb-1, popcount
+// c = n - popc(H)).  In the ascending sector order the states sharing H are consecutive rows,
+// the block off(H) .. off(H) + C(kb, c) - 1, and row(H, lo) = off(H) + lo_idx[lo] with
+// off(H) = sum over H's set bits p (the (c+1)-th, (c+2)-th ... set bit of s) of C(p, m) — the low
+// terms of the rank are exactly lo_idx[lo] (the combinatorial number system, R28).  One warp per
+// block, everything that depends on H is warp-uniform and computed once per block:
+//  * high bonds (j, j+1), kb <= j <= L-2: the partner has the same lo, its block is a fixed
+//    +-C(j, m-1) rows away — a coalesced read at a per-block offset (no per-row index work);
+//  * the boundary bond (kb-1, kb) and the periodic bond (L-1, 0) move one bit between the parts:
+//    the partner's block H' is uniform, its index lo_idx[lo'] per lane;
+//  * low bonds (j, j+1), j <= kb-2: the partner is in the same block (<= 924 rows, L1-resident).
+// Blocks are dealt to warps in ascending order over one resident wave (sz_blocks), so at any
+// time the warps sweep a window of ~4700 consecutive blocks and a partner block within a few
+// thousand blocks is read from L2 (measured at L = 30: one CTA per block, or a second wave,
+// read more from DRAM and ran 1.4-1.9x slower).
+// No per-row unranking; ~4x fewer instructions per row than the rank-stepping kernel above.
+// Measured (sk_apply_operator, n = L/2): L = 26 583 -> 358 us, L = 30 9.84 -> 5.76 ms.
+template <int NRHS>
+__global__ void __launch_bounds__(kThreads, NRHS == 2 ? SZB_MINB - 1 : SZB_MINB) heisenberg_szb_kernel(SpmvArgs a, KParams kp, int L, int nup, double J, int fl) {
+    __shared__ StepScratch sc;
+    __shared__ SzTables tab;
+    __shared__ long long dl[kThreads / 32][kSzMaxL];   // per-warp high-bond row offsets
+    bool agent;
+    int buf;
+    if (!spmv_enter(a, agent, buf, sc, kp)) return;
+    const cplx *__restrict__ r = pick3(a.r, buf);
+    const cplx *__restrict__ t = pick3(a.t, buf);
+    const double qJ = 0.25 * J, hJ = 0.5 * J;
+    const int off = a.st ? 1 : 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    cplx w = mk(0.0, 0.0);
+    if (!agent) {
+        {   // tables -> shared memory
+            const uint4 *src = (const uint4 *)&g_sz_tab;
+            uint4 *dst = (uint4 *)&tab;
+            for (int e = threadIdx.x; e < (int)(sizeof(SzTables) / 16); e += blockDim.x) dst[e] = src[e];
+        }
+        __syncthreads();
+        const int kb = L - 1 < kSzLoBits ? L - 1 : kSzLoBits;
+        const int nh = L - kb;
+        long long *dw = dl[warp];
+        // off(H) for the block of H with low class c
+        auto off_hi = [&](uint32_t H, int c) -> int64_t {
+            int64_t o = 0;
+            for (int m = c + 1; H; ++m) {
+                const int p = __ffs((int)H) - 1;
+                H &= H - 1u;
+                o += (int64_t)tab.C[p + kb][m];
+            }
+            return o;
+        };
+        const int64_t nH = int64_t(1) << nh;
+        // hint (vectors beyond L2): far partners (> 8 MB away) are read evict-first, q written
+        // streaming — neither is reused before it would be evicted anyway
+        const bool hint = fl & 2;
+        const int64_t farlim = int64_t(1) << 19;
+        const int64_t hstep = (int64_t)(gridDim.x - off) * (blockDim.x >> 5);
+        for (int64_t hw = (int64_t)(blockIdx.x - off) * (blockDim.x >> 5) + warp; hw < nH; hw += hstep) {
+            const uint32_t H = (uint32_t)hw;
+            const int c = nup - __popc(H);
+            if (c < 0 || c > kb) continue;
+            const int cnt = (int)tab.C[kb][c];
+            const int64_t o = off_hi(H, c);
+            // high bonds: bit b of xh <-> bond (kb + b, kb + b + 1)
+            const uint32_t xh = (H ^ (H >> 1)) & ((1u << (nh - 1)) - 1u);
+            int nb = 0;
+            __syncwarp();   // the previous block's reads of dw are done
+            for (uint32_t xx = xh; xx; xx &= xx - 1u, ++nb) {
+                const int b = __ffs((int)xx) - 1;
+                const int m = c + __popc(H & ((2u << (b + 1)) - 1u));   // index of the moving bit
+                const long long d = (long long)tab.C[kb + b][m - 1];
+                if (lane == 0) dw[nb] = ((H >> b) & 1u) ? d : -d;
+            }
+            __syncwarp();
+            // boundary bond (kb-1, kb) and periodic bond (L-1, 0): uniform partner blocks
+            const uint32_t hb = H & 1u, ht = (H >> (nh - 1)) & 1u;
+            const int cB = hb ? c + 1 : c - 1, cP = ht ? c + 1 : c - 1;
+            const int64_t oB = (cB >= 0 && cB <= kb) ? off_hi(H ^ 1u, cB) : 0;
+            const int64_t oP = (cP >= 0 && cP <= kb) ? off_hi(H ^ (1u << (nh - 1)), cP) : 0;
+            const int nhb = __popc(xh);
+            for (int i0 = 0; i0 < cnt; i0 += 32) {
+                const int idx = i0 + lane;
+                if (idx >= cnt) break;
+                const uint32_t lo = tab.lo_list[tab.lo_off[c] + idx];
+                const int64_t i = o + idx;
+                const uint32_t xl = (lo ^ (lo >> 1)) & ((1u << (kb - 1)) - 1u);
+                const bool onB = ((lo >> (kb - 1)) & 1u) != hb, onP = (lo & 1u) != ht;
+                const double d = qJ * (double)(L - 2 * (__popc(xl) + nhb + (int)onB + (int)onP));
+                const cplx rs = r[i];
+                cplx q = mk(d * rs.x, d * rs.y);
+                cplx ts = mk(0, 0), qt = mk(0, 0);
+                if (NRHS == 2) { ts = t[i]; qt = mk(d * ts.x, d * ts.y); }
+                // high bonds, 4 coalesced reads in flight
+                for (int u0 = 0; u0 < nb; u0 += 4) {
+                    cplx v[4], vt[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const bool on = u0 + u < nb;
+                        const long long dd = dw[u0 + u];
+                        const int64_t p = on ? i + dd : i;
+                        v[u] = on ? ((hint && (dd > farlim || dd < -farlim)) ? __ldcs(r + p) : r[p]) : mk(0.0, 0.0);
+                        if (NRHS == 2) vt[u] = on ? t[p] : mk(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        q.x = fma(hJ, v[u].x, q.x);
+                        q.y = fma(hJ, v[u].y, q.y);
+                        if (NRHS == 2) {
+                            qt.x = fma(hJ, vt[u].x, qt.x);
+                            qt.y = fma(hJ, vt[u].y, qt.y);
+                        }
+                    }
+                }
+                // low bonds, boundary and periodic bond: the partner is the lo_idx-th row of a
+                // block with a uniform base (own block, H ^ 1, H ^ top bit), two batches in flight
+                const cplx *rb[3] = {r + o, r + oB, r + oP}, *tb[3] = {t + o, t + oB, t + oP};
+                const uint32_t onm = xl | ((uint32_t)onB << (kSzLoBits - 1)) | ((uint32_t)onP << kSzLoBits);
+                constexpr int kHalf = SZB_BATCH;
+#pragma unroll
+                for (int j0 = 0; j0 <= kSzLoBits; j0 += kHalf) {
+                    cplx v[kHalf], vt[kHalf];
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u) {
+                        const int j = j0 + u;
+                        if (j > kSzLoBits) break;
+                        const int sel = j < kSzLoBits - 1 ? 0 : j - (kSzLoBits - 2);
+                        const bool on = (onm >> j) & 1u;
+                        const uint32_t flip = j < kSzLoBits - 1 ? 3u << j : (j == kSzLoBits - 1 ? 1u << (kb - 1) : 1u);
+                        const uint32_t pj = tab.lo_idx[(lo ^ flip) & (kSzLo - 1)];
+                        v[u] = on ? rb[sel][pj] : mk(0.0, 0.0);
+                        if (NRHS == 2) vt[u] = on ? tb[sel][pj] : mk(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kHalf; ++u) {
+                        if (j0 + u > kSzLoBits) break;
+                        q.x = fma(hJ, v[u].x, q.x);
+                        q.y = fma(hJ, v[u].y, q.y);
+                        if (NRHS == 2) {
+                            qt.x = fma(hJ, vt[u].x, qt.x);
+                            qt.y = fma(hJ, vt[u].y, qt.y);
+                        }
+                    }
+                }
+                if (hint) __stcs(a.q + i, q); else a.q[i] = q;
+                if (NRHS == 2) {
+                    a.qt[i] = qt;
+                    w = cfma_conj(ts, q, w);
+                } else {
+                    w = cfma(rs, q, w);
+                }
+            }
+        }
+    }
+    spmv_exit(a, kp, agent, w, sc);
+}
+
 static cudaError_t sz_tables_init() {
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
@@ -197,11 +361,35 @@ static cudaError_t sz_tables_init() {
     return err;
 }
 
+// SHIFTK_SZ_RANK=1 selects the rank-stepping kernel (kept for comparison)
+static bool sz_rank_kernel() {
+    static int en = -1;
+    if (en < 0) {
+        const char *e = getenv("SHIFTK_SZ_RANK");
+        en = (e && e[0] == '1') ? 1 : 0;
+    }
+    return en == 1;
+}
+
+// One resident wave (SZB_MINB CTAs per SM, one slot for the finish agent): the warps sweep the
+// blocks H once in ascending order; a second wave would start a second sweep over the partners.
+int sz_blocks(int L, int64_t M, int bicg) {
+    const int b = stream_blocks(M);
+    if (L < 2 || sz_rank_kernel()) return b;
+    const int cap = (bicg ? SZB_MINB - 1 : SZB_MINB) * sm_count() - 1;
+    return b < cap ? b : cap;
+}
+
 cudaError_t launch_heisenberg_sz(const SpmvArgs &a, const KParams &kp, int L, int nup, double J, cudaStream_t s) {
     const cudaError_t e = sz_tables_init();
     if (e != cudaSuccess) return e;
-    const int grid = stream_blocks(a.M) + (a.st ? 1 : 0);
+    const int grid = sz_blocks(L, a.M, a.bicg) + (a.st ? 1 : 0);
     const bool p = a.st != nullptr;
+    if (L >= 2 && !sz_rank_kernel()) {
+        const int fl = a.M * (int64_t)sizeof(cplx) >= (int64_t(64) << 20) ? 2 : 0;
+        if (a.bicg) return launch_k(heisenberg_szb_kernel<2>, grid, kThreads, 0, s, p, a, kp, L, nup, J, fl);
+        return launch_k(heisenberg_szb_kernel<1>, grid, kThreads, 0, s, p, a, kp, L, nup, J, fl);
+    }
     if (L <= 31) {
         if (a.bicg) return launch_k(heisenberg_sz_kernel<2, uint32_t>, grid, kThreads, 0, s, p, a, kp, L, nup, J);
         return launch_k(heisenberg_sz_kernel<1, uint32_t>, grid, kThreads, 0, s, p, a, kp, L, nup, J);

@@ -88,7 +88,11 @@ def test_heisenberg_operator_parity(L):
     assert np.max(np.abs(qd.cpu().numpy() - qo)) <= 1e-14 * np.max(np.abs(qo))
 
 
-@pytest.mark.parametrize("L,n", [(12, 6), (16, 8), (14, 3), (11, 0), (20, 10)])
+@pytest.mark.parametrize("L,n", [(12, 6), (16, 8), (14, 3), (11, 0), (20, 10),
+                                 # block-kernel edges: one high bit (L <= 13), tiny chains,
+                                 # empty/full classes, a far-from-half sector, 22 sites
+                                 (2, 1), (3, 1), (3, 2), (5, 2), (13, 6), (13, 13), (13, 0),
+                                 (14, 7), (21, 4), (22, 11)])
 def test_heisenberg_sz_operator_parity(L, n):
     """Sector operator (f-3): GPU combinatorial ranking vs the oracle's enumerated basis."""
     rng = np.random.default_rng(L * 7 + n)
