@@ -420,6 +420,13 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
                 kp.wred_off = nt <= sk::kStreamDirect ? 0 : nt;
                 kp.wred_n = (int32_t)(nt <= sk::kStreamDirect ? nt : ng);
             }
+            if (H->kind == SK_OP_HEISENBERG_SZ && sk::sz_partials(H->L) > 0) {   // per block + per group
+                const int64_t nt = int64_t(1) << (H->L - std::min(H->L - 1, 12));
+                np = std::max<int64_t>(np, sk::sz_partials(H->L));
+                ng = std::max<int64_t>(1, (nt + sk::kStreamGroup - 1) / sk::kStreamGroup);
+                kp.wred_off = nt <= sk::kStreamDirect ? 0 : nt;
+                kp.wred_n = (int32_t)(nt <= sk::kStreamDirect ? nt : ng);
+            }
             // deferred seed step on one GPU with the built-in operator: two halves (iteration
             // parity), because the next SpMV writes its partials while the finish reads these
             kp.defer = (world == 1 && H->kind != SK_OP_RC) ? 1 : 0;
@@ -1036,11 +1043,9 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
     a.part_w = nullptr;
     a.bicg = 0;
     cudaStream_t s = (cudaStream_t)stream;
-    if (H->kind == SK_OP_HEISENBERG) {
-        if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L)) return fail(SK_EINVAL, "L/M");
-        a.M = H->M;
-        // tile queue of the streaming kernel: one zeroed pair per device, rewound by the kernel
-        // itself (stand-alone calls on one device must not run concurrently)
+    if (H->kind == SK_OP_HEISENBERG || H->kind == SK_OP_HEISENBERG_SZ) {
+        // work queue of the streaming / sector kernels: one zeroed pair per device, rewound by
+        // the kernel itself (stand-alone calls on one device must not run concurrently)
         static unsigned long long *work[sk::kMaxWorld] = {};
         int dev = 0;
         CK(cudaGetDevice(&dev));
@@ -1050,6 +1055,10 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
             CK(cudaMemset(work[dev], 0, 2 * sizeof(unsigned long long)));
         }
         a.work = work[dev];
+    }
+    if (H->kind == SK_OP_HEISENBERG) {
+        if (H->L < 1 || H->L > 34 || H->M != (int64_t(1) << H->L)) return fail(SK_EINVAL, "L/M");
+        a.M = H->M;
         CK(sk::launch_heisenberg(a, KParams{}, H->L, H->J, s));
     } else if (H->kind == SK_OP_HEISENBERG_SZ) {
         if (H->L < 1 || H->L > 34 || H->n_up < 0 || H->n_up > H->L || H->M < 1)

@@ -44,7 +44,8 @@ constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
 
 int stream_blocks(int64_t M);
 int heisenberg_blocks(int L, int64_t M, int bicg);   // worker CTAs (= partials) of the Heisenberg SpMV
-int sz_blocks(int L, int64_t M, int bicg);                     // worker CTAs of the sector SpMV
+int sz_blocks(int L, int64_t M, int bicg);
+int64_t sz_partials(int L);                          // w partials of the sector SpMV (0: per CTA)                     // worker CTAs of the sector SpMV
 bool heis_stream(int L, int64_t M, int bicg);      // the TMA-fed streaming kernel is used
 bool heis_pairs(int L, int64_t M);                 // ... as tile pairs across the top spin bit (one GPU)
 int sm_count();

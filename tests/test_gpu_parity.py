@@ -112,6 +112,27 @@ def test_heisenberg_sz_window():
     run_window(synth.make_problem("c5sz", L=16, nz=64), 20)
 
 
+def test_heisenberg_sz_window_grouped_partials():
+    """26 sites, Sz = 0 (C(26,13) = 10,400,600 rows, 2^14 high-bit blocks): the block kernel's
+    queue-dealt blocks and its per-block + per-group w partials (more than kStreamDirect blocks)."""
+    run_window(synth.make_problem("c5sz", L=26, nz=8), 4)
+
+
+def test_heisenberg_sz_queue_order_is_bitwise_irrelevant():
+    """The sector SpMV deals blocks from a queue (the order differs launch to launch), but w is
+    summed per block and per group in index order: sk_run == stepwise, bit for bit."""
+    p = synth.make_problem("c5sz", L=26, nz=8)
+    dp = to_device(p)
+    a = make_solver(dp)
+    b = make_solver(dp)
+    for _ in range(12):
+        a.update()
+    b.run(12, poll_every=5)
+    assert np.array_equal(a.residuals(), b.residuals())
+    assert np.array_equal(a.projections(), b.projections())
+    assert a.coefficients() == b.coefficients()
+
+
 def test_heisenberg_ferromagnet_bit_exact_gpu():
     L = 20
     op = shiftk.make_operator({"kind": "heisenberg", "L": L, "J": 1.0}, 1 << L)
