@@ -225,7 +225,9 @@ int sk_get_coefficients(sk_ctx *ctx, sk_coeffs *out);
 int sk_finalize(sk_ctx **ctx);
 
 /* q = H r for the given operator on device vectors (no solver state); for operator parity
-   tests.  stream: cudaStream_t or NULL (default stream). */
+   tests.  stream: cudaStream_t or NULL (default stream).  The Heisenberg (streaming) and
+   Heisenberg-sector kernels take their work from a per-device queue that each launch rewinds:
+   calls for those operators on one device must not run concurrently on different streams. */
 int sk_apply_operator(const sk_operator *H, const sk_cplx *r_dev, sk_cplx *q_dev, void *stream);
 
 /* ---- contour-integral eigensolver building blocks ----------
