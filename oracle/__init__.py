@@ -176,6 +176,23 @@ def apply_rows(op: dict, r: np.ndarray, rows) -> np.ndarray:
     return out
 
 
+def heisenberg_sz_row_fn(L: int, n: int, J: float, rfun, a: int) -> complex:
+    """(H r)_a on the sector with r given as a function of the row index (for vectors too large
+    to hold on the host): the sum over the L bonds (i, i+1 mod L) of J S_i.S_j, P:L1048-1054 —
+    +J/4 r_a if the spins are parallel, else -J/4 r_a + J/2 r_{rank(s with both flipped)} — in
+    the same order as or_heisenberg_sz_row (pinned against it in tests/test_oracle_pins.py)."""
+    s = sz_unrank(L, n, a)
+    acc = 0j
+    for i in range(L):
+        j = (i + 1) % L
+        if ((s >> i) & 1) == ((s >> j) & 1):
+            acc += 0.25 * J * rfun(a)
+        else:
+            acc += -0.25 * J * rfun(a)
+            acc += 0.5 * J * rfun(sz_rank(L, s ^ ((1 << i) | (1 << j))))
+    return acc
+
+
 def apply_op(op: dict, r: np.ndarray) -> np.ndarray:
     """q = H r with the oracle's own operator code."""
     if op["kind"] == "heisenberg":

@@ -152,3 +152,41 @@ def test_c5sz_full_size_sector_operator_sampled_rows():
     del qd, rd
     qo = oracle.apply_rows({"kind": "heisenberg_sz", "L": L, "n_up": n, "J": 1.0}, r, rows)
     assert np.max(np.abs(q_rows - qo) / np.maximum(np.abs(qo), 1e-300)) <= 1e-13
+
+
+def _hash_vec_np(k):
+    """r_k from an integer hash of the row index (20-bit fractions: exact in fp64 on both sides)."""
+    k = np.asarray(k, dtype=np.int64)
+    re = ((k * 2654435761) & 0xFFFFF).astype(np.float64) / 1048576.0 - 0.5
+    im = (((k * 40503 + 12345) >> 3) & 0xFFFFF).astype(np.float64) / 1048576.0 - 0.5
+    return re + 1j * im
+
+
+def test_sector_operator_beyond_2_31_rows_sampled():
+    """L = 34, Sz = 0: C(34,17) = 2,333,606,220 rows (> 2^31; 37 GB per vector), the block
+    kernel's 64-bit row and block offsets.  r_k is an integer hash of k, generated on the GPU in
+    chunks and evaluated by the oracle's row routine as a function (the vector does not fit on
+    the host); sampled rows incl. the first, last and around 2^31."""
+    L, n = 34, 17
+    D = math.comb(L, n)
+    rd = torch.empty(D, dtype=torch.complex128, device="cuda")
+    ch = 1 << 27
+    for k0 in range(0, D, ch):
+        k = torch.arange(k0, min(D, k0 + ch), dtype=torch.int64, device="cuda")
+        re = ((k * 2654435761) & 0xFFFFF).to(torch.float64) / 1048576.0 - 0.5
+        im = (((k * 40503 + 12345) >> 3) & 0xFFFFF).to(torch.float64) / 1048576.0 - 0.5
+        rd[k0:k0 + k.shape[0]] = torch.complex(re, im)
+        del k, re, im
+    qd = torch.empty_like(rd)
+    op = shiftk.make_operator({"kind": "heisenberg_sz", "L": L, "J": 1.0, "n_up": n}, D)
+    shiftk.apply_operator(op, rd, qd)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(34)
+    rows = [0, 1, (1 << 31) - 1, 1 << 31, (1 << 31) + 1, D // 2, D - 2, D - 1] + list(rng.integers(0, D, 24))
+    q_rows = qd[torch.tensor(rows, device="cuda")].cpu().numpy()
+    assert np.array_equal(rd[torch.tensor(rows[:4], device="cuda")].cpu().numpy(), _hash_vec_np(rows[:4]))
+    del qd, rd
+    torch.cuda.empty_cache()
+    qo = np.array([oracle.heisenberg_sz_row_fn(L, n, 1.0, lambda k: complex(_hash_vec_np(k)), a) for a in rows])
+    # |q_a| <= (L/4 + L/2) max|r|; rounding of a 35-term sum is ~1e-15 of that
+    assert np.max(np.abs(q_rows - qo)) <= 1e-13

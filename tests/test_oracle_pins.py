@@ -524,6 +524,19 @@ def test_sz_sampled_rows_match_the_full_product():
     assert np.array_equal(oracle.apply_rows(op, r, rows), q[rows])
 
 
+def test_sz_row_fn_matches_the_full_product():
+    """heisenberg_sz_row_fn (r as a function of the row) = the list-based product, row by row
+    (it serves the L = 34 GPU check, whose vector does not fit on the host)."""
+    L, n = 13, 6
+    rng = np.random.default_rng(13)
+    D = oracle.sz_dim(L, n)
+    r = rng.standard_normal(D) + 1j * rng.standard_normal(D)
+    q = oracle.heisenberg_sz_apply(L, n, 0.7, r)
+    rows = [0, 1, 2, 100, D // 2, D - 2, D - 1]
+    got = np.array([oracle.heisenberg_sz_row_fn(L, n, 0.7, lambda k: r[k], a) for a in rows])
+    assert np.max(np.abs(got - q[rows])) <= 1e-14 * np.max(np.abs(q))
+
+
 def test_sz_sector_solver_matches_dense_solve():
     """Shifted COCG on the sector operator (the same oracle solver) converges to the dense
     sector solve: y_k = b^dagger (z_k - H_sector)^-1 b."""
