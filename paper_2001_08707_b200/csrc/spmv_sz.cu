@@ -5,7 +5,9 @@
 // i-th one.  rank(s) = sum over the set bits of s, taken in ascending position p_1 < p_2 < ...,
 // of C(p_m, m) (the states below s, counted by their highest differing bit).
 //
-// One thread per sector row, consecutive rows on consecutive lanes:
+// Two kernels: the block-structured heisenberg_szb_kernel (default, described above it) and the
+// earlier rank-stepping heisenberg_sz_kernel (SHIFTK_SZ_RANK=1, kept for comparison), which runs
+// one thread per sector row, consecutive rows on consecutive lanes:
 //  * unranking — lane 0 of a warp unranks the warp's first row bit by bit from the top; the
 //    other lanes step from it inside the block of states that share the bits >= 12: there the
 //    12 low bits run through the 12-bit patterns with a fixed popcount in ascending order, a
