@@ -112,6 +112,33 @@ def test_heisenberg_sz_window():
     run_window(synth.make_problem("c5sz", L=16, nz=64), 20)
 
 
+def test_rank_stepping_sector_kernel_still_matches():
+    """The earlier rank-stepping sector kernel (SHIFTK_SZ_RANK=1, read once per process, so in a
+    subprocess): operator parity and a short solver window (per-CTA w partials)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, synth, oracle\n"
+        "from paper_2001_08707_b200 import shiftk\n"
+        "from test_gpu_parity import run_window\n"
+        "for L, n in [(16, 8), (14, 3), (13, 13)]:\n"
+        "    D = oracle.sz_dim(L, n)\n"
+        "    r = np.random.default_rng(L).standard_normal(D) + 0.5j\n"
+        "    op = shiftk.make_operator({'kind': 'heisenberg_sz', 'L': L, 'J': 1.0, 'n_up': n}, D)\n"
+        "    rd = torch.from_numpy(r).cuda(); qd = torch.empty_like(rd)\n"
+        "    shiftk.apply_operator(op, rd, qd); torch.cuda.synchronize()\n"
+        "    qo = oracle.heisenberg_sz_apply(L, n, 1.0, r)\n"
+        "    assert np.max(np.abs(qd.cpu().numpy() - qo)) <= 1e-14 * np.max(np.abs(qo)), (L, n)\n"
+        "run_window(synth.make_problem('c5sz', L=16, nz=16), 10)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SHIFTK_SZ_RANK="1", PYTHONPATH=root + os.pathsep + os.path.join(root, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
+
+
 def test_heisenberg_sz_window_grouped_partials():
     """26 sites, Sz = 0 (C(26,13) = 10,400,600 rows, 2^14 high-bit blocks): the block kernel's
     queue-dealt blocks and its per-block + per-group w partials (more than kStreamDirect blocks)."""
