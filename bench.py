@@ -11,8 +11,8 @@ a=b projection, COCG, complex128.
 
 Timing: W untimed iterations, then K iterations each bracketed by CUDA events on the solver's
 stream, with L2 flushed (256 MiB write) before every step outside the events; barrier +
-synchronize around the timed region; max over ranks.  Clocks are sampled with nvidia-smi
-during the timed region.  `value` comes from a pass with nothing between the kernels; a second
+synchronize around the timed region; max over ranks.  Clocks are sampled with NVML every 2 ms
+(nvidia-smi where NVML is missing) during the timed region.  `value` comes from a pass with nothing between the kernels; a second
 pass of the same K flushed steps records CUDA events around every kernel (on the solver's
 stream) for the per-kernel durations behind `roofline` (events between the kernels cost the
 programmatic-launch overlap, ~10 us per step at C2, so that pass is not the value).  `--impl reference` times the CPU oracle (oracle/) on the same
@@ -77,17 +77,43 @@ def bytes_per_row(problem, kernel: str) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region.
+
+    NVML (pynvml) polled every 2 ms from a thread, so even a few-ms timed region gets several
+    samples; nvidia-smi (-lms 100) where NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
+        self.period = period_s
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []     # (sm_mhz, sm_max_mhz, {reason names}) from NVML
+        self.stop = threading.Event()
+        self.source = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.bits = [pynvml.nvmlClocksEventReasonHwSlowdown,
+                         pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwPowerCap]
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.nvml, self.h = pynvml, h
+            self._sample_nvml()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            self.source = "nvml"
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
@@ -95,15 +121,36 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            self.source = "nvidia-smi"
         except OSError:
             self.proc = None
         return self
+
+    def _sample_nvml(self):
+        nv = self.nvml
+        sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((sm, self.smax, {n for n, b in zip(self.NAMES, self.bits) if r & b}))
+
+    def _poll(self):
+        while not self.stop.wait(self.period):
+            try:
+                self._sample_nvml()
+            except Exception:
+                return
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=5)
+            try:
+                self._sample_nvml()      # the end of the timed region (after its synchronize)
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -113,7 +160,10 @@ class ClockSampler:
 
     def summary(self):
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s_, m_, r_ in self.samples:
+            sm.append(s_)
+            smax = m_
+            reasons |= r_
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
@@ -123,11 +173,11 @@ class ClockSampler:
                 smax = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:6]):
+            for n, v in zip(self.NAMES, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 # ------------------------------------------------------------------------------ oracle legs
