@@ -16,10 +16,13 @@ int shift_agents(int nz) {
     return a < 1 ? 1 : (a > 8 ? 8 : a);
 }
 
+#ifndef UPD_MINB
+#define UPD_MINB 4
+#endif
 int update_blocks(int64_t M, int nl, int full, int nz) {
     const int R = 1;   // rows per thread per chunk (the non-full kernel pipelines two chunks)
     int64_t b = (M + (int64_t)kThreads * R - 1) / ((int64_t)kThreads * R);
-    const int64_t cap = 148 * 4 - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
+    const int64_t cap = 148 * UPD_MINB - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
@@ -102,7 +105,7 @@ static __device__ __forceinline__ bool update_seed(const KParams &kp, UpdSeed &u
 // Each thread owns R rows per sweep (rows tid, tid+256, ... of a 256*R chunk) and issues all of
 // their loads before any arithmetic, so 4R+ independent 16-byte loads are in flight per thread.
 template <int NLMAX, bool BICG, bool FULL, int R>
-__global__ void __launch_bounds__(kThreads, FULL ? 2 : 4)
+__global__ void __launch_bounds__(kThreads, FULL ? 2 : UPD_MINB)
 update_kernel(KParams kp, const cplx *__restrict__ q, const cplx *__restrict__ qt) {
     extern __shared__ cplx dyn[];  // FULL: coef[3 nz], flags[nz], list[nz]
     __shared__ ShiftScratch ss;
