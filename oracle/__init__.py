@@ -25,6 +25,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "shiftk_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP_PATH = os.path.join(_HERE, "liboracle_omp.so")
 
 COCG, BICG = 0, 1
 ITERATING, CONVERGED, MAXITER, BREAKDOWN = 0, 1, 2, 3
@@ -33,22 +34,36 @@ STATUS_NAMES = {0: "iterating", 1: "converged", 2: "maxiter", 3: "breakdown"}
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with plain gcc (no fast-math, no BLAS)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-fno-fast-math",
-                               "-ffp-contract=off", "-o", _LIB_PATH, _SRC, "-lm"])
+    """Compile the oracle with plain gcc (no fast-math, no BLAS): liboracle.so (one thread) and
+    liboracle_omp.so (-fopenmp; the same order of every floating-point operation, so the same
+    bits — see the header of shiftk_oracle.c)."""
+    for path, extra in ((_LIB_PATH, []), (_LIB_OMP_PATH, ["-fopenmp"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+            tmp = path + ".tmp"
+            subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-fno-fast-math",
+                                   "-ffp-contract=off"] + extra + ["-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, path)
     return _LIB_PATH
 
 
-_lib = None
+_libs = {}
 _c128p = ctypes.c_void_p
+# default build for the module-level functions and Oracle(): ORACLE_OMP=1 selects the OpenMP one
+_DEFAULT_OMP = os.environ.get("ORACLE_OMP", "0") == "1"
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        _lib = ctypes.CDLL(build())
-        L = _lib
+def threads() -> int:
+    """Threads the OpenMP build uses (OMP_NUM_THREADS, else the host's cores)."""
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n else (os.cpu_count() or 1)
+
+
+def lib(omp: Optional[bool] = None):
+    omp = _DEFAULT_OMP if omp is None else bool(omp)
+    if omp not in _libs:
+        build()
+        _libs[omp] = ctypes.CDLL(_LIB_OMP_PATH if omp else _LIB_PATH)
+        L = _libs[omp]
         L.or_create.restype = ctypes.c_void_p
         L.or_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _c128p, _c128p,
                                 ctypes.c_int64, _c128p, ctypes.c_int, ctypes.c_double,
@@ -98,26 +113,29 @@ def lib():
         L.or_heisenberg_sz_row.restype = _C
         L.or_heisenberg_sz_row.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, _c128p,
                                            ctypes.c_int64]
-    return _lib
+    return _libs[omp]
 
 
 def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
-def _view(addr: int, n: int, dtype) -> np.ndarray:
-    """Copy n elements of dtype from a C pointer."""
+def _view(addr: int, n: int, dtype, copy: bool = True) -> np.ndarray:
+    """n elements of dtype at a C pointer: a copy, or (copy=False) a view valid until the
+    oracle's next call that moves the buffer."""
     dt = np.dtype(dtype)
     buf = (ctypes.c_char * (n * dt.itemsize)).from_address(addr)
-    return np.frombuffer(buf, dtype=dt, count=n).copy()
+    a = np.frombuffer(buf, dtype=dt, count=n)
+    return a.copy() if copy else a
 
 
 # ------------------------------------------------------------------------------- operators
 
-def heisenberg_apply(L: int, J: float, r: np.ndarray) -> np.ndarray:
+def heisenberg_apply(L: int, J: float, r: np.ndarray, out: Optional[np.ndarray] = None,
+                     omp: Optional[bool] = None) -> np.ndarray:
     r = np.ascontiguousarray(r, dtype=np.complex128)
-    q = np.empty_like(r)
-    lib().or_heisenberg_apply(L, J, _ptr(r), _ptr(q))
+    q = np.empty_like(r) if out is None else out
+    lib(omp).or_heisenberg_apply(L, J, _ptr(r), _ptr(q))
     return q
 
 
@@ -149,11 +167,12 @@ def heisenberg_sz_apply(L: int, n: int, J: float, r: np.ndarray) -> np.ndarray:
     return q
 
 
-def csr_apply(op: dict, r: np.ndarray) -> np.ndarray:
+def csr_apply(op: dict, r: np.ndarray, out: Optional[np.ndarray] = None,
+              omp: Optional[bool] = None) -> np.ndarray:
     r = np.ascontiguousarray(r, dtype=np.complex128)
-    q = np.empty_like(r)
+    q = np.empty_like(r) if out is None else out
     M = op["row_ptr"].shape[0] - 1
-    fn = lib().or_csr_real_apply if op["kind"] == "csr_real" else lib().or_csr_cplx_apply
+    fn = lib(omp).or_csr_real_apply if op["kind"] == "csr_real" else lib(omp).or_csr_cplx_apply
     fn(M, _ptr(op["row_ptr"]), _ptr(op["col"]), _ptr(op["val"]), _ptr(r), _ptr(q))
     return q
 
@@ -193,13 +212,18 @@ def heisenberg_sz_row_fn(L: int, n: int, J: float, rfun, a: int) -> complex:
     return acc
 
 
-def apply_op(op: dict, r: np.ndarray) -> np.ndarray:
-    """q = H r with the oracle's own operator code."""
+def apply_op(op: dict, r: np.ndarray, out: Optional[np.ndarray] = None,
+             omp: Optional[bool] = None) -> np.ndarray:
+    """q = H r with the oracle's own operator code (into ``out`` when given)."""
     if op["kind"] == "heisenberg":
-        return heisenberg_apply(op["L"], op["J"], r)
+        return heisenberg_apply(op["L"], op["J"], r, out, omp)
     if op["kind"] == "heisenberg_sz":
-        return heisenberg_sz_apply(op["L"], op["n_up"], op["J"], r)
-    return csr_apply(op, r)
+        q = heisenberg_sz_apply(op["L"], op["n_up"], op["J"], r)
+        if out is not None:
+            out[...] = q
+            return out
+        return q
+    return csr_apply(op, r, out, omp)
 
 
 # ------------------------------------------------------------------------------- solver
@@ -210,7 +234,12 @@ class Oracle:
 
     def __init__(self, method: str, b: np.ndarray, z: np.ndarray, *, left: Optional[np.ndarray] = None,
                  full_x: bool = False, tol: float = 1e-10, itermax: int = 10000, flags: int = 0,
-                 keep: Optional[np.ndarray] = None):
+                 keep: Optional[np.ndarray] = None, omp: Optional[bool] = None):
+        """b and left are borrowed by the C state: this object keeps references to them.
+        omp selects the OpenMP build (bit-identical results; default: ORACLE_OMP env)."""
+        self._h = None
+        self.omp = _DEFAULT_OMP if omp is None else bool(omp)
+        self._q = self._qt = None   # reused H r / H t buffers of step()
         self.method = COCG if method == "cocg" else BICG
         self.b = np.ascontiguousarray(b, dtype=np.complex128)
         self.z = np.ascontiguousarray(z, dtype=np.complex128)
@@ -220,16 +249,19 @@ class Oracle:
         self.full_x = bool(full_x)
         self._keep = None if keep is None else np.ascontiguousarray(keep, dtype=np.uint8)
         self.tol = tol
-        self._h = lib().or_create_subset(self.method, self.M, self.nz, _ptr(self.z), _ptr(self.b),
+        self._h = self._lib().or_create_subset(self.method, self.M, self.nz, _ptr(self.z), _ptr(self.b),
                                          self.nleft, 0 if self.left is None else _ptr(self.left),
                                          int(self.full_x), float(tol), int(itermax), int(flags),
                                          0 if self._keep is None else _ptr(self._keep))
         if not self._h:
             raise ValueError("oracle init rejected its arguments")
 
+    def _lib(self):
+        return lib(self.omp)
+
     def close(self):
         if self._h:
-            lib().or_destroy(self._h)
+            self._lib().or_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -237,27 +269,38 @@ class Oracle:
 
     # reverse communication -----------------------------------------------------------
     def r(self) -> np.ndarray:
-        return _view(lib().or_r(self._h), self.M, np.complex128)
+        return _view(self._lib().or_r(self._h), self.M, np.complex128)
 
     def r_old(self) -> np.ndarray:
-        return _view(lib().or_r_old(self._h), self.M, np.complex128)
+        return _view(self._lib().or_r_old(self._h), self.M, np.complex128)
 
     def t(self) -> np.ndarray:
-        return _view(lib().or_t(self._h), self.M, np.complex128)
+        return _view(self._lib().or_t(self._h), self.M, np.complex128)
 
     def update(self, q: np.ndarray, qt: Optional[np.ndarray] = None) -> int:
+        """Reverse communication: the caller supplies q = H r (and qt = H t for BiCG)."""
         q = np.ascontiguousarray(q, dtype=np.complex128)
         qt_p = 0
         if self.method == BICG:
             qt = np.ascontiguousarray(qt, dtype=np.complex128)
             qt_p = _ptr(qt)
-        return lib().or_update(self._h, _ptr(q), qt_p)
+        return self._lib().or_update(self._h, _ptr(q), qt_p)
 
     def step(self, op: dict) -> int:
-        """One iteration with the oracle's own operator: q = H r (and H t for BiCG), update."""
-        q = apply_op(op, self.r())
-        qt = apply_op(op, self.t()) if self.method == BICG else None
-        return self.update(q, qt)
+        """One iteration with the oracle's own operator: q = H r (and H t for BiCG), update.
+        r is read in place and q lives in a buffer reused from step to step (no M-vector copy)."""
+        if self.status != ITERATING:
+            return self.status
+        if self._q is None:
+            self._q = np.empty(self.M, dtype=np.complex128)
+        L_ = self._lib()
+        apply_op(op, _view(L_.or_r(self._h), self.M, np.complex128, copy=False), self._q, self.omp)
+        qt = None
+        if self.method == BICG:
+            if self._qt is None:
+                self._qt = np.empty(self.M, dtype=np.complex128)
+            qt = apply_op(op, _view(L_.or_t(self._h), self.M, np.complex128, copy=False), self._qt, self.omp)
+        return self.update(self._q, qt)
 
     def run(self, op: dict, max_iters: int) -> int:
         st = self.status
@@ -270,47 +313,47 @@ class Oracle:
     # getters -------------------------------------------------------------------------
     @property
     def status(self) -> int:
-        return lib().or_status(self._h)
+        return self._lib().or_status(self._h)
 
     @property
     def iterations(self) -> int:
-        return lib().or_iterations(self._h)
+        return self._lib().or_iterations(self._h)
 
     @property
     def switches(self) -> int:
-        return lib().or_switches(self._h)
+        return self._lib().or_switches(self._h)
 
     @property
     def spmv_count(self) -> int:
-        return lib().or_spmv_count(self._h)
+        return self._lib().or_spmv_count(self._h)
 
     @property
     def seed_index(self) -> int:
-        return lib().or_seed_index(self._h)
+        return self._lib().or_seed_index(self._h)
 
     def residuals(self) -> np.ndarray:
-        return _view(lib().or_res(self._h), self.nz, np.float64)
+        return _view(self._lib().or_res(self._h), self.nz, np.float64)
 
     def active(self) -> np.ndarray:
-        return _view(lib().or_active(self._h), self.nz, np.uint8).astype(bool)
+        return _view(self._lib().or_active(self._h), self.nz, np.uint8).astype(bool)
 
     def retired_at(self) -> np.ndarray:
-        return _view(lib().or_retired_at(self._h), self.nz, np.int64)
+        return _view(self._lib().or_retired_at(self._h), self.nz, np.int64)
 
     def pi(self) -> np.ndarray:
-        return _view(lib().or_pi(self._h), self.nz, np.complex128)
+        return _view(self._lib().or_pi(self._h), self.nz, np.complex128)
 
     def pi_old(self) -> np.ndarray:
-        return _view(lib().or_pi_old(self._h), self.nz, np.complex128)
+        return _view(self._lib().or_pi_old(self._h), self.nz, np.complex128)
 
     def projections(self) -> np.ndarray:
         """y[k, l] = a_l^dagger x^(k) from the projected recurrences."""
-        return _view(lib().or_y(self._h), self.nz * self.nleft, np.complex128).reshape(self.nz, self.nleft)
+        return _view(self._lib().or_y(self._h), self.nz * self.nleft, np.complex128).reshape(self.nz, self.nleft)
 
     def solution(self, k: int) -> np.ndarray:
         if not self.full_x:
             raise ValueError("full x not stored")
-        addr = lib().or_x(self._h, k)
+        addr = self._lib().or_x(self._h, k)
         if not addr:
             raise ValueError(f"x of shift {k} not carried (keep mask)")
         return _view(addr, self.M, np.complex128)
@@ -320,17 +363,17 @@ class Oracle:
         z_new = np.ascontiguousarray(z_new, dtype=np.complex128)
         y = np.zeros((z_new.shape[0], self.nleft), dtype=np.complex128)
         res = np.zeros(z_new.shape[0], dtype=np.float64)
-        lib().or_recalc(self._h, z_new.shape[0], _ptr(z_new), float(self.tol if tol is None else tol),
+        self._lib().or_recalc(self._h, z_new.shape[0], _ptr(z_new), float(self.tol if tol is None else tol),
                         _ptr(y), res.ctypes.data)
         return y, res
 
     @property
     def log_length(self) -> int:
-        return lib().or_log_length(self._h)
+        return self._lib().or_log_length(self._h)
 
     def scalars(self) -> dict:
         out = np.zeros(6, dtype=np.complex128)
-        lib().or_scalars(self._h, _ptr(out))
+        self._lib().or_scalars(self._h, _ptr(out))
         return dict(alpha=out[0], beta=out[1], rho=out[2], w=out[3], z_seed=out[4], alpha_prev=out[5])
 
 

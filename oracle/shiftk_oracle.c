@@ -7,9 +7,20 @@
  * and bench.py's cpu_baseline / --impl reference legs may load this library.  It shares no
  * code, header, table or helper with the CUDA path (paper_2001_08707_b200/csrc).
  *
- * Arithmetic: IEEE fp64, C99 `double complex`, every reduction a fixed-order loop over
- * i = 0..M-1 (or M-1..0 with OR_FLAG_REVERSE, used only to measure the self-divergence
- * horizon of SURVEY §8(c.4)).  Single-threaded.
+ * Arithmetic: IEEE fp64, C99 `double complex`.  Every reduction has one fixed order: the
+ * index range is cut into consecutive chunks of OR_CHUNK elements, each chunk is summed in
+ * index order, and the chunk sums are added in index order (SURVEY §8(c.1) "Determinism": "a
+ * static chunking, accumulates per chunk in order, and combines the chunks in index order").
+ * OR_FLAG_REVERSE runs both levels backwards (used only to measure the self-divergence
+ * horizon of SURVEY §8(c.4)).  The same source is built twice: liboracle.so (one thread) and
+ * liboracle_omp.so (-fopenmp: the chunks and the element-wise loops are shared out among
+ * threads).  The order of every floating-point operation is the same in both, so the two
+ * builds give bit-identical results (pinned in tests/test_oracle_pins.py).
+ *
+ * Memory: b and the left vectors are BORROWED (the caller keeps them alive until or_destroy);
+ * with a = b the single left vector is b itself.  r_{n+1} is formed in the buffer of r_{n-1}
+ * (each element is read before it is overwritten), so the state holds three M-vectors (r, r_old
+ * and, for BiCG, t, t_old) beyond b — the paper's three-vector storage.
  *
  * Algorithm (one call of or_update = one iteration n; step numbers follow SURVEY §8(c.1)):
  *   inner product  <u,v> = sum u_i v_i (COCG, App. A)  |  sum conj(u_i) v_i (BiCG)
@@ -47,11 +58,16 @@
  */
 #include <complex.h>
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
 typedef double complex cplx;
+
+#define OR_CHUNK 32768   /* reduction chunk (elements) */
 
 enum { OR_COCG = 0, OR_BICG = 1 };
 enum { OR_ITERATING = 0, OR_CONVERGED = 1, OR_MAXITER = 2, OR_BREAKDOWN = 3 };
@@ -61,8 +77,10 @@ typedef struct {
     int method, full, flags;
     int64_t M, nz, nleft, itermax;
     double tol;
-    cplx *b, *left;            /* left: [nleft][M] (copy of b when a = b) */
-    cplx *r, *r_old, *t, *t_old, *tmp;
+    const cplx *b, *left;      /* borrowed; left: [nleft][M] (b itself when a = b) */
+    cplx *r, *r_old, *t, *t_old;
+    cplx *part;                /* chunk sums of one reduction */
+    int64_t nchunk;
     cplx *z, zs;
     int64_t s;
     cplx *pi, *pi_old, *pi_new;
@@ -84,24 +102,40 @@ typedef struct {
 
 /* ------------------------------------------------------------------ inner products */
 
-static cplx dot_plain(const or_state *st, const cplx *u, const cplx *v) {
+/* sum over i of f(u_i, v_i) in the fixed chunked order (see the header); conj_u selects
+   conj(u_i) v_i instead of u_i v_i */
+static cplx dot_chunked(const or_state *st, const cplx *u, const cplx *v, int conj_u) {
+    const int64_t M = st->M, nc = st->nchunk;
+    const int rev = (st->flags & OR_FLAG_REVERSE) != 0;
+    cplx *part = st->part;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t i0 = c * OR_CHUNK, i1 = (i0 + OR_CHUNK < M) ? i0 + OR_CHUNK : M;
+        cplx acc = 0;
+        if (rev) {
+            for (int64_t i = i1 - 1; i >= i0; --i) acc += (conj_u ? conj(u[i]) : u[i]) * v[i];
+        } else {
+            for (int64_t i = i0; i < i1; ++i) acc += (conj_u ? conj(u[i]) : u[i]) * v[i];
+        }
+        part[c] = acc;
+    }
     cplx acc = 0;
-    if (st->flags & OR_FLAG_REVERSE) {
-        for (int64_t i = st->M - 1; i >= 0; --i) acc += u[i] * v[i];
+    if (rev) {
+        for (int64_t c = nc - 1; c >= 0; --c) acc += part[c];
     } else {
-        for (int64_t i = 0; i < st->M; ++i) acc += u[i] * v[i];
+        for (int64_t c = 0; c < nc; ++c) acc += part[c];
     }
     return acc;
 }
 
+static cplx dot_plain(const or_state *st, const cplx *u, const cplx *v) {
+    return dot_chunked(st, u, v, 0);
+}
+
 static cplx dot_conj(const or_state *st, const cplx *u, const cplx *v) {
-    cplx acc = 0;
-    if (st->flags & OR_FLAG_REVERSE) {
-        for (int64_t i = st->M - 1; i >= 0; --i) acc += conj(u[i]) * v[i];
-    } else {
-        for (int64_t i = 0; i < st->M; ++i) acc += conj(u[i]) * v[i];
-    }
-    return acc;
+    return dot_chunked(st, u, v, 1);
 }
 
 /* <u, v> of the method: unconjugated for COCG (App. A), conjugated for BiCG (App. B) */
@@ -143,11 +177,13 @@ or_state *or_create_subset(int method, int64_t M, int64_t nz, const cplx *z, con
     st->method = method; st->M = M; st->nz = nz; st->full = full; st->tol = tol;
     st->itermax = itermax; st->flags = flags;
     st->nleft = left ? nleft : 1;
-    st->b = (cplx *)xcalloc(M, sizeof(cplx));
-    st->left = (cplx *)xcalloc(st->nleft * M, sizeof(cplx));
-    st->r = (cplx *)xcalloc(M, sizeof(cplx));
+    st->b = b;
+    st->left = left ? left : b;
+    st->nchunk = (M + OR_CHUNK - 1) / OR_CHUNK;
+    st->part = (cplx *)xcalloc(st->nchunk, sizeof(cplx));
+    st->r = (cplx *)malloc((size_t)M * sizeof(cplx));
     st->r_old = (cplx *)xcalloc(M, sizeof(cplx));
-    st->tmp = (cplx *)xcalloc(M, sizeof(cplx));
+    if (!st->r || !st->r_old || !st->part) { or_destroy(st); return NULL; }
     if (method == OR_BICG) {
         st->t = (cplx *)xcalloc(M, sizeof(cplx));
         st->t_old = (cplx *)xcalloc(M, sizeof(cplx));
@@ -174,14 +210,11 @@ or_state *or_create_subset(int method, int64_t M, int64_t nz, const cplx *z, con
         st->x = (cplx *)xcalloc((size_t)(nkeep * M), sizeof(cplx));
         if (!st->p || !st->x) { or_destroy(st); return NULL; }
     }
-    memcpy(st->b, b, M * sizeof(cplx));
     memcpy(st->z, z, nz * sizeof(cplx));
-    if (left) memcpy(st->left, left, nleft * M * sizeof(cplx));
-    else memcpy(st->left, b, M * sizeof(cplx));
 
     /* Init: r_0 = b, r_{-1} = 0, t_0 = conj(b) (R3), pi_0 = pi_{-1} = 1,
        x_0 = 0, y_0 = 0, first seed z[0]. */
-    memcpy(st->r, b, M * sizeof(cplx));
+    memcpy(st->r, b, (size_t)M * sizeof(cplx));
     if (method == OR_BICG)
         for (int64_t i = 0; i < M; ++i) st->t[i] = conj(b[i]);
     double nb = sqrt(creal(dot_conj(st, b, b)));
@@ -196,7 +229,7 @@ or_state *or_create_subset(int method, int64_t M, int64_t nz, const cplx *z, con
 
 void or_destroy(or_state *st) {
     if (!st) return;
-    free(st->b); free(st->left); free(st->r); free(st->r_old); free(st->tmp);
+    free(st->part); free(st->r); free(st->r_old);
     free(st->t); free(st->t_old); free(st->z); free(st->pi); free(st->pi_old); free(st->pi_new);
     free(st->active); free(st->res); free(st->retired_at); free(st->g); free(st->u); free(st->y);
     free(st->p); free(st->x); free(st->keep);
@@ -272,22 +305,38 @@ int or_update(or_state *st, const cplx *q, const cplx *qt) {
             int64_t slot = 0;
             for (int64_t j = 0; j < k; ++j) slot += st->keep[j];
             cplx *p = st->p + slot * M, *x = st->x + slot * M;
+            const cplx *rr = st->r, ipk = st->pi[k];
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
             for (int64_t i = 0; i < M; ++i) {
-                p[i] = st->r[i] / st->pi[k] + bk * p[i];
+                p[i] = rr[i] / ipk + bk * p[i];
                 x[i] = x[i] + ak * p[i];
             }
         }
     }
 
-    /* 8 */
-    for (int64_t i = 0; i < M; ++i)
-        st->tmp[i] = (1.0 + c) * st->r[i] - alpha * (st->zs * st->r[i] - q[i]) - c * st->r_old[i];
-    { cplx *o = st->r_old; st->r_old = st->r; st->r = st->tmp; st->tmp = o; }
+    /* 8  (r_{n+1} formed in the buffer of r_{n-1}: element i of r_{n-1} is read before it is
+          overwritten, then the buffers rotate) */
+    {
+        cplx *rn = st->r, *ro = st->r_old;
+        const cplx zs = st->zs;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+        for (int64_t i = 0; i < M; ++i)
+            ro[i] = (1.0 + c) * rn[i] - alpha * (zs * rn[i] - q[i]) - c * ro[i];
+        st->r = ro; st->r_old = rn;
+    }
     if (bicg) {
         cplx cc = conj(c), ac = conj(alpha), zc = conj(st->zs);
+        cplx *tn = st->t, *to = st->t_old;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
         for (int64_t i = 0; i < M; ++i)
-            st->tmp[i] = (1.0 + cc) * st->t[i] - ac * (zc * st->t[i] - qt[i]) - cc * st->t_old[i];
-        cplx *o = st->t_old; st->t_old = st->t; st->t = st->tmp; st->tmp = o;
+            to[i] = (1.0 + cc) * tn[i] - ac * (zc * tn[i] - qt[i]) - cc * to[i];
+        st->t = to; st->t_old = tn;
     }
 
     /* 9 */
@@ -323,10 +372,18 @@ int or_update(or_state *st, const cplx *q, const cplx *qt) {
         }
         if (best != st->s) {
             cplx f = st->pi[best], fp = st->pi_old[best];
-            for (int64_t i = 0; i < M; ++i) { st->r[i] /= f; st->r_old[i] /= fp; }
+            cplx *rr = st->r, *ro = st->r_old;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+            for (int64_t i = 0; i < M; ++i) { rr[i] /= f; ro[i] /= fp; }
             if (bicg) {
                 cplx fc = conj(f), fpc = conj(fp);
-                for (int64_t i = 0; i < M; ++i) { st->t[i] /= fc; st->t_old[i] /= fpc; }
+                cplx *tt = st->t, *to = st->t_old;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+                for (int64_t i = 0; i < M; ++i) { tt[i] /= fc; to[i] /= fpc; }
             }
             for (int64_t k = 0; k < nz; ++k) {
                 if (!st->active[k]) continue;
@@ -391,6 +448,9 @@ int64_t or_log_length(const or_state *st) { return st->nlog; }
    anti-aligned pair with amplitude J/2. */
 void or_heisenberg_apply(int L, double J, const cplx *r, cplx *q) {
     const int64_t M = (int64_t)1 << L;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
     for (int64_t s = 0; s < M; ++s) {
         cplx acc = 0;
         for (int i = 0; i < L; ++i) {
@@ -411,6 +471,9 @@ void or_heisenberg_apply(int L, double J, const cplx *r, cplx *q) {
 /* q = H r for a CSR matrix with real values (row_ptr int64[M+1], col int32[nnz]). */
 void or_csr_real_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, const double *val,
                        const cplx *r, cplx *q) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
     for (int64_t i = 0; i < M; ++i) {
         cplx acc = 0;
         for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
@@ -421,6 +484,9 @@ void or_csr_real_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, co
 /* q = H r for a CSR matrix with complex values. */
 void or_csr_cplx_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, const cplx *val,
                        const cplx *r, cplx *q) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
     for (int64_t i = 0; i < M; ++i) {
         cplx acc = 0;
         for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
@@ -433,13 +499,14 @@ void or_csr_cplx_apply(int64_t M, const int64_t *row_ptr, const int32_t *col, co
 cplx or_heisenberg_row(int L, double J, const cplx *r, int64_t s) {
     cplx acc = 0;
     for (int i = 0; i < L; ++i) {
-        int j = (i + 1) % L;
-        int bi = (int)((s >> i) & 1), bj = (int)((s >> j) & 1);
+        const int j = (i + 1) % L;                    /* bond (i, i+1 mod L) */
+        const int bi = (int)((s >> i) & 1), bj = (int)((s >> j) & 1);
         if (bi == bj) {
-            acc += 0.25 * J * r[s];
+            acc += 0.25 * J * r[s];                   /* parallel spins: +J/4 */
         } else {
-            acc += -0.25 * J * r[s];
-            acc += 0.5 * J * r[s ^ (((int64_t)1 << i) | ((int64_t)1 << j))];
+            const int64_t flip = ((int64_t)1 << i) | ((int64_t)1 << j);
+            acc += -0.25 * J * r[s];                  /* antiparallel: -J/4 */
+            acc += 0.5 * J * r[s ^ flip];             /* and J/2 to the flipped pair */
         }
     }
     return acc;
@@ -447,15 +514,17 @@ cplx or_heisenberg_row(int L, double J, const cplx *r, int64_t s) {
 
 cplx or_csr_real_row(const int64_t *row_ptr, const int32_t *col, const double *val, const cplx *r,
                      int64_t i) {
+    const int64_t e_begin = row_ptr[i], e_end = row_ptr[i + 1];
     cplx acc = 0;
-    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
+    for (int64_t e = e_begin; e < e_end; ++e) acc += val[e] * r[col[e]];      /* real row */
     return acc;
 }
 
 cplx or_csr_cplx_row(const int64_t *row_ptr, const int32_t *col, const cplx *val, const cplx *r,
                      int64_t i) {
+    const int64_t e_begin = row_ptr[i], e_end = row_ptr[i + 1];
     cplx acc = 0;
-    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) acc += val[e] * r[col[e]];
+    for (int64_t e = e_begin; e < e_end; ++e) acc += val[e] * r[col[e]];      /* complex row */
     return acc;
 }
 

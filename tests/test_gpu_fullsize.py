@@ -1,14 +1,21 @@
 """GPU parity at BASELINE.json's FULL sizes (C3, C4, C5), in the launch configuration bench.py
 times, on what the oracle can afford there:
 
-* C3 (M = 2^24, 128 shifts, full x): the first iterations against the oracle, all residuals and
-  projections compared, x^(k) compared for two carried shifts (the oracle's keep mask: its
+* C3 (M = 2^24, 128 shifts, full x): the first n_w iterations against the oracle, all residuals
+  and projections compared, x^(k) compared for two carried shifts (the oracle's keep mask: its
   scalar recurrences and seed switching still run over all 128 shifts);
-* C4 (8192^2 lattice, 64 contour points, 32 left vectors, BiCG): first iterations, all 64 x 32
-  projections and residuals;
-* C5 (L = 30, 2^30 states) and its Sz = 0 sector (f-3): sampled rows of H r against the oracle's row routine, the
+* C4 (8192^2 lattice, 64 contour points, 32 left vectors, BiCG): first n_w iterations, all
+  64 x 32 projections and residuals;
+* C5 (L = 30, 2^30 states, 512 shifts, a = b): the first iterations against the oracle (all
+  512 residuals and projections), sampled rows of H r against the oracle's row routine, the
   ferromagnet H 1 = (L/4) 1 bit-exactly, and exact termination after 3 iterations for a
-  right-hand side with 3 distinct energies (closed-form G(z)) — properties that hold at any size.
+  right-hand side with 3 distinct energies (closed-form G(z)) — properties that hold at any size;
+  its Sz = 0 sector (f-3): sampled rows.
+
+Window length: n_w = min(cap, self-divergence horizon), the horizon measured
+on a scaled instance of the same geometry (tests/horizon.py; two oracle runs at full size would
+double the cost).  The oracle runs its OpenMP build here (bit-identical to the one-thread build,
+tests/test_oracle_pins.py::test_openmp_build_is_bit_identical) on the host's cores.
 """
 import math
 
@@ -17,6 +24,7 @@ import pytest
 
 import oracle
 import synth
+from horizon import horizon_of
 
 pytestmark = pytest.mark.gpu
 
@@ -38,7 +46,7 @@ def window(p, n_w, keep=None, check_x=()):
     dp = to_device(p)
     g = make_solver(dp)
     o = oracle.Oracle(p.method, p.b, p.z, left=p.left, full_x=p.full_x, tol=p.tol,
-                      itermax=p.itermax, keep=keep)
+                      itermax=p.itermax, keep=keep, omp=True)
     for n in range(n_w):
         assert g.update() == o.step(p.op) == shiftk.ITERATING
         rg, ro = g.residuals(), o.residuals()
@@ -61,21 +69,38 @@ def sampled_rows(p, dp, r, rows):
 
 
 def test_c3_full_size():
+    n_w = min(20, horizon_of("c3", 20, M=1 << 14))
+    assert n_w >= 10, n_w
     p = synth.make_problem("c3")
     keep = np.zeros(p.n_shift, dtype=np.uint8)
     keep[[5, 77]] = 1
-    dp, g = window(p, 4, keep=keep, check_x=(5, 77))
+    dp, g = window(p, n_w, keep=keep, check_x=(5, 77))
     rows = np.random.default_rng(7).integers(0, p.M, 64)
     sampled_rows(p, dp, p.b, rows)
 
 
 def test_c4_full_size():
+    n_w = min(12, horizon_of("c4", 12, W=64))
+    assert n_w >= 8, n_w
     p = synth.make_problem("c4")
-    dp, g = window(p, 3)
+    dp, g = window(p, n_w)
     c = g.coefficients()
-    assert c["spmv_count"] == 2 * c["iterations"] == 6
+    assert c["spmv_count"] == 2 * c["iterations"] == 2 * n_w
     rows = np.random.default_rng(8).integers(0, p.M, 64)
     sampled_rows(p, dp, p.left[3], rows)
+
+
+def test_c5_full_size_window():
+    """C5 exactly as bench.py times it (L = 30, M = 2^30, 512 shifts w + 0.05i in [-16, 4), a = b,
+    the single-GPU pair / split SpMV and the fused update): the first iterations against the
+    oracle on all 512 shifts, 1e-9 on residuals and projections."""
+    n_w = min(5, horizon_of("c5", 5, L=18))
+    assert n_w == 5
+    p = synth.make_problem("c5")
+    dp, g = window(p, n_w)
+    assert g.coefficients()["iterations"] == n_w
+    del dp, g, p
+    torch.cuda.empty_cache()
 
 
 def _popcount(a):

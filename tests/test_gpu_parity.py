@@ -3,8 +3,9 @@
 Protocol:
   * trajectory window: per iteration n <= n_w and per shift, |dres|/res <= 1e-9 and the
     normwise projection error max_l|dy_kl| / max_l|y_kl| <= 1e-9 (R23); the seed index and
-    the retirement iterations agree.  n_w is chosen below the self-divergence horizon of two
-    correct fp64 orderings (measured in test_self_divergence_horizon).
+    the retirement iterations agree.  n_w = min(cap, horizon): the self-divergence horizon of
+    two correct fp64 orderings of the oracle (tests/horizon.py), measured on
+    the test's own input; the cap bounds the oracle's cost.
   * converged: per-shift projection error <= 1e-9; every residual below tol on both sides.
 """
 import math
@@ -14,6 +15,7 @@ import pytest
 
 import oracle
 import synth
+from horizon import horizon
 
 pytestmark = pytest.mark.gpu
 
@@ -34,7 +36,9 @@ def proj_err(a, b):
     return num / den
 
 
-def run_window(problem, n_w, *, full_check=False, flags=0, tol=None):
+def run_window(problem, n_cap, *, full_check=False, flags=0, tol=None):
+    n_w = horizon(problem, n_cap, flags=flags, tol=tol)
+    assert n_w >= min(n_cap, 3), ("self-divergence horizon too short", n_w)
     dp = to_device(problem)
     g = make_solver(dp, flags=flags, tol=tol)
     o = oracle.Oracle(problem.method, problem.b, problem.z, left=problem.left,
@@ -453,6 +457,49 @@ def test_recalc_parity(name, kw):
     # then report a residual above tol, of the same size)
     assert np.all((rg < p.tol) == (ro < p.tol)) or np.all(np.abs(np.log10(rg / ro)) < 1)
     assert g.coefficients()["spmv_count"] == g.coefficients()["iterations"] * (2 if p.method == "bicg" else 1)
+
+
+@pytest.mark.parametrize("name,kw", [("c1", dict(L=10, nz=8)), ("c2", dict(L=14, nz=64)),
+                                     ("c4", dict(W=12, nz=8, n_left=4))])
+def test_checkpoint_restart_matches_oracle(name, kw):
+    """Restart ("restart coefficients supplied at init", P:L575 calctype=restart; SURVEY
+    f-4) against the ORACLE: k iterations, checkpoint, the context destroyed, a fresh context
+    restored from the blob; the restored state equals the oracle's after k iterations, and the
+    restored context then advances in lockstep with the uninterrupted oracle run through the
+    rest of the trajectory window (1e-9 on residuals and projections, equal retirement
+    iterations, active sets and seed; full x compared in full mode)."""
+    p = synth.make_problem(name, **kw)
+    n_w = horizon(p, 40)
+    assert n_w >= 10, n_w
+    k = n_w // 2
+    dp = to_device(p)
+    a = make_solver(dp)
+    a.run(k)
+    blob = a.checkpoint()
+    a.finalize()
+    del a
+    g = make_solver(dp)
+    g.restore(blob)
+    o = oracle.Oracle(p.method, p.b, p.z, left=p.left, full_x=p.full_x, tol=p.tol, itermax=p.itermax)
+    for _ in range(k):
+        o.step(p.op)
+    for n in range(k, n_w + 1):
+        if n > k:
+            assert g.update() == o.step(p.op), n
+        rg, ro = g.residuals(), o.residuals()
+        assert np.all(np.abs(rg - ro) <= REL * ro), (n, np.max(np.abs(rg - ro) / ro))
+        assert np.all(proj_err(g.projections(), o.projections()) <= REL), n
+        c = g.coefficients()
+        assert c["iterations"] == o.iterations == n
+        if c["seed_index"] != o.seed_index:   # a |pi| tie (conjugate contour pairs): see run_window
+            pio = np.abs(o.pi())
+            assert abs(pio[c["seed_index"]] / pio[o.seed_index] - 1) < 1e-9, n
+        _, act, ret = g.shift_state()
+        assert np.array_equal(act, o.active()) and np.array_equal(ret, o.retired_at()), n
+        if p.full_x:
+            for kk in (0, p.n_shift - 1):
+                xo = o.solution(kk)
+                assert np.linalg.norm(g.solution(kk) - xo) <= REL * np.linalg.norm(xo), (n, kk)
 
 
 @pytest.mark.parametrize("name,kw", [("c1", dict(L=10, nz=8)), ("c4", dict(W=12, nz=8, n_left=4))])

@@ -194,11 +194,12 @@ def _lanczos(Hmul, b, n):
     return np.array(al), np.array(be)
 
 
-def test_cocg_is_lanczos_fom():
+@pytest.mark.parametrize("L", [10, 17])
+def test_cocg_is_lanczos_fom(L):
     """COCG with real-symmetric H, real b is Lanczos-FOM (SURVEY §0 finding 3):
     b^T x_n(z) = ||b||^2 [(z - T_n)^{-1}]_{11};  pi_n^k = chi_n(z_k)/chi_n(z_seed);
-    ||r_n^(k)|| = ||b|| prod_{j<=n} beta_j / |chi_n(z_k)|, chi_n(z) = det(z - T_n)."""
-    L = 10
+    ||r_n^(k)|| = ||b|| prod_{j<=n} beta_j / |chi_n(z_k)|, chi_n(z) = det(z - T_n).
+    L = 17 (2^17 rows) spans four reduction chunks of the oracle (OR_CHUNK = 2^15)."""
     p = synth.make_problem("c2", L=L, nz=24)
     Hmul = lambda v: oracle.heisenberg_apply(L, 1.0, v)
     al, be = _lanczos(Hmul, p.b, 26)
@@ -237,10 +238,11 @@ def test_cocg_orthogonality_and_projection_zero():
             assert abs(np.vdot(p.b, rs[i])) / np.linalg.norm(rs[i]) < 1e-12
 
 
-def test_bicg_biorthogonality():
+@pytest.mark.parametrize("W", [10, 200])
+def test_bicg_biorthogonality(W):
     """App. B: t_i^dagger r_j = 0 (i != j), t_i^dagger r_i != 0; complex b so the
-    shadow sequence is not a multiple of r."""
-    p = synth.make_problem("c4", W=10, nz=6, n_left=1)
+    shadow sequence is not a multiple of r.  W = 200 (40000 rows) spans two reduction chunks."""
+    p = synth.make_problem("c4", W=W, nz=6, n_left=1)
     rng = np.random.default_rng(11)
     b = rng.standard_normal(p.M) + 1j * rng.standard_normal(p.M)
     b /= np.linalg.norm(b)
@@ -613,3 +615,82 @@ def test_ss_moments_are_the_quadrature_filter_of_the_spectrum():
     assert inside.sum() >= 2
     far = np.abs(np.abs(lam + 4.0) - 0.6) > 0.1
     assert np.all(np.abs(f0[inside & far] - 1) < 1e-3) and np.all(np.abs(f0[~inside & far]) < 1e-3)
+
+
+# ----------------------------------------------------------------------------- row routines
+
+@pytest.mark.parametrize("L", [12, 13])
+def test_heisenberg_row_routine_matches_the_full_product(L):
+    """or_heisenberg_row (the checker behind every sampled-row GPU test at L = 30) against the
+    full product or_heisenberg_apply, which is pinned above by Table 3, the
+    ferromagnet and the magnon dispersion: every row, a complex random vector (a wrong flip
+    partner or bond would move most rows)."""
+    rng = np.random.default_rng(100 + L)
+    M = 1 << L
+    r = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    op = {"kind": "heisenberg", "L": L, "J": 1.0}
+    full = oracle.apply_op(op, r)
+    rows = np.arange(M)
+    assert np.array_equal(oracle.apply_rows(op, r, rows), full)
+    # and directly against the bond sum of P:L831 written out for a handful of rows
+    for s in (0, 1, M - 1, M // 3, 0b1011 % M):
+        acc = 0j
+        for i in range(L):
+            j = (i + 1) % L
+            if ((s >> i) & 1) == ((s >> j) & 1):
+                acc += 0.25 * r[s]
+            else:
+                acc += -0.25 * r[s] + 0.5 * r[s ^ ((1 << i) | (1 << j))]
+        assert abs(oracle.apply_rows(op, r, [s])[0] - acc) <= 1e-14 * abs(acc)
+
+
+@pytest.mark.parametrize("kind,kw", [("c3", dict(M=1 << 12)), ("c4", dict(W=24, nz=4, n_left=1))])
+def test_csr_row_routines_match_scipy(kind, kw):
+    """or_csr_real_row / or_csr_cplx_row (the checkers of the sampled C3/C4 rows) against the
+    scipy.sparse product on the same CSR arrays (an independent library routine), every row."""
+    p = synth.make_problem(kind, **kw)
+    rng = np.random.default_rng(7)
+    r = rng.standard_normal(p.M) + 1j * rng.standard_normal(p.M)
+    want = sp.csr_matrix((p.op["val"], p.op["col"], p.op["row_ptr"]), shape=(p.M, p.M)) @ r
+    got = oracle.apply_rows(p.op, r, np.arange(p.M))
+    assert np.max(np.abs(got - want)) <= 1e-14 * np.max(np.abs(want))
+
+
+# ----------------------------------------------------------------------------- OpenMP build
+
+@pytest.mark.parametrize("name,kw", [("c1", dict(L=16, nz=6)), ("c4", dict(W=190, nz=4, n_left=3))])
+def test_openmp_build_is_bit_identical(name, kw):
+    """liboracle_omp.so (the reference arm's all-core oracle) performs the same floating-point
+    operations in the same order as liboracle.so: residuals, projections, r and x agree bit for
+    bit after 30 iterations (sizes spanning several reduction chunks; seed switches included)."""
+    p = synth.make_problem(name, **kw)
+    a = oracle.Oracle(p.method, p.b, p.z, left=p.left, full_x=p.full_x, tol=p.tol, itermax=500, omp=False)
+    b = oracle.Oracle(p.method, p.b, p.z, left=p.left, full_x=p.full_x, tol=p.tol, itermax=500, omp=True)
+    for _ in range(30):
+        assert a.step(p.op) == b.step(p.op)
+    assert a.switches == b.switches > 0
+    assert np.array_equal(a.residuals(), b.residuals())
+    assert np.array_equal(a.projections(), b.projections())
+    assert np.array_equal(a.r(), b.r())
+    if p.full_x:
+        assert np.array_equal(a.solution(2), b.solution(2))
+
+
+# ----------------------------------------------------------------------------- horizon tool
+
+def test_self_divergence_horizon_tool():
+    """tests/horizon.py: two correct orderings of the oracle agree to 1e-12 for
+    a few dozen iterations (~40 for C1's geometry), then drift apart — the tool finds a finite
+    horizon there, and reports the whole run for an input that terminates exactly (3 energies)."""
+    from horizon import horizon
+    p = synth.make_problem("c1")
+    h = horizon(p, 200)
+    assert 25 <= h < 200, h
+    # agreement really fails right after the horizon: the two runs differ by more than 1e-12
+    a = oracle.Oracle(p.method, p.b, p.z, tol=p.tol, itermax=p.itermax)
+    b = oracle.Oracle(p.method, p.b, p.z, tol=p.tol, itermax=p.itermax, flags=oracle.FLAG_REVERSE)
+    for _ in range(h + 1):
+        a.step(p.op); b.step(p.op)
+    d = max(np.max(np.abs(a.residuals() - b.residuals()) / a.residuals()),
+            np.max(np.abs(a.projections() - b.projections()) / np.abs(a.projections())))
+    assert d > 1e-12 or not np.array_equal(a.retired_at(), b.retired_at())

@@ -13,13 +13,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 SRC = os.path.join(ROOT, "oracle", "shiftk_oracle.c")
 
 MUTATIONS = [
-    ("- c * st->r_old[i]", "+ c * st->r_old[i]"),                       # sign, EQ-CG-RN-3REC
+    ("- c * ro[i]", "+ c * ro[i]"),                                       # sign, EQ-CG-RN-3REC
     ("rat * rat * beta", "rat * beta"),                                   # EQ-SHIFTEDCG-beta square
     ("- w - gamma * rho", "- w"),                                         # EQ-REC-ALPHA-N2 term
     ("- c * st->pi_old[k];", ";"),                                        # EQ-SHIFTEDCG-PI term
     ("*u = st->g[l] / st->pi[k]", "*u = st->g[l] / pin"),                # P:L373 index
     ("acc += 0.25 * J * r[s];", "acc += 0.5 * J * r[s];"),               # S^zS^z factor
-    ("(1.0 + cc) * st->t[i] - ac", "(1.0 + c) * st->t[i] - ac"),         # BiCG shadow conj
+    ("(1.0 + cc) * tn[i] - ac", "(1.0 + c) * tn[i] - ac"),               # BiCG shadow conj
     ("st->rho_prev /= fp * fp;", "st->rho_prev /= fp;"),                 # switch transform
     ("st->alpha_prev *= fp / f;", "st->alpha_prev *= f / fp;"),          # switch transform
     ("OR_COCG ? dot_plain(st, u, v)", "OR_COCG ? dot_conj(st, u, v)"),   # COCG inner product
@@ -30,6 +30,15 @@ MUTATIONS = [
     ("if (rank >= below) {", "if (rank > below) {"),                     # sector unrank
     ("rank += or_sz_dim(p, m);", "rank += or_sz_dim(p, m - 1);"),        # sector rank
     ("acc += 0.25 * J * r[a];", "acc += 0.25 * J * r[s];"),              # sector row vs state
+    # row routines (the checkers of the sampled full-size GPU rows)
+    ("acc += 0.5 * J * r[s ^ flip];", "acc += 0.5 * J * r[s ^ ((int64_t)1 << i)];"),   # row flip partner
+    ("const int j = (i + 1) % L;                    /* bond", "const int j = (i + 1 < L) ? i + 1 : i; /* bond"),
+    ("acc += val[e] * r[col[e]];      /* real row */", "acc += val[e] * r[i];      /* real row */"),  # CSR gather
+    ("acc += val[e] * r[col[e]];      /* complex row */", "acc += conj(val[e]) * r[col[e]];      /* complex row */"),
+    # the chunked fixed-order reduction and the in-place three-term update
+    ("for (int64_t c = 0; c < nc; ++c) acc += part[c];", "for (int64_t c = 0; c + 1 < nc; ++c) acc += part[c];"),
+    ("? i0 + OR_CHUNK : M;", "? i0 + OR_CHUNK - 1 : M;"),
+    ("st->r = ro; st->r_old = rn;", "st->r = ro; st->r_old = ro;"),
     # contour-integral eigensolver (oracle/ss.py)
     ("s += (z[j] - gamma) / n_z * (z[j] - gamma) ** k * X[l, j]",
      "s += 1.0 / n_z * (z[j] - gamma) ** k * X[l, j]", "ss.py"),        # dz weight
