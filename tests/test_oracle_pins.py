@@ -679,8 +679,8 @@ def test_openmp_build_is_bit_identical(name, kw):
 # ----------------------------------------------------------------------------- horizon tool
 
 def test_self_divergence_horizon_tool():
-    """tests/horizon.py: two correct orderings of the oracle agree to 1e-12 for
-    a few dozen iterations (~40 for C1's geometry), then drift apart — the tool finds a finite
+    """tests/horizon.py: two correct orderings of the oracle agree to 1e-11 for
+    a few dozen iterations (31 for C1's geometry), then drift apart — the tool finds a finite
     horizon there, and reports the whole run for an input that terminates exactly (3 energies)."""
     from horizon import horizon
     p = synth.make_problem("c1")
@@ -693,4 +693,4 @@ def test_self_divergence_horizon_tool():
         a.step(p.op); b.step(p.op)
     d = max(np.max(np.abs(a.residuals() - b.residuals()) / a.residuals()),
             np.max(np.abs(a.projections() - b.projections()) / np.abs(a.projections())))
-    assert d > 1e-12 or not np.array_equal(a.retired_at(), b.retired_at())
+    assert d > 1e-11 or not np.array_equal(a.retired_at(), b.retired_at())
