@@ -256,7 +256,10 @@ static int group_iteration(sk_group *g) {
     return group_allreduce(g, true);
 }
 
+// (every context entry point reaches the device through here or read_state: both select the
+// context's device first, so a caller whose current device differs is served correctly)
 static int enqueue_finish(sk_ctx *c) {
+    CK(cudaSetDevice(c->device));
     if (!c->pending_host) return SK_OK;
     CK(sk::launch_scalar(c->kp, sk::PH_FINISH, c->stream));
     c->launches += 1;
@@ -265,6 +268,7 @@ static int enqueue_finish(sk_ctx *c) {
 }
 
 static int read_state(sk_ctx *c) {
+    CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SK_OK;
@@ -995,6 +999,7 @@ int sk_profile_enable(sk_ctx *c, int32_t on) {
 
 int sk_get_profile(sk_ctx *c, sk_profile *o, int32_t reset) {
     if (!c || !o) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
     // events come in groups of 3 per iteration: [spmv (+finish, +seed)] [update (+shift step)]
     const size_t groups = c->ev_used / 3;
@@ -1022,6 +1027,7 @@ int sk_get_profile(sk_ctx *c, sk_profile *o, int32_t reset) {
 int sk_debug_timestamps(sk_ctx *c, int64_t *out16) {
     if (!c || !out16) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
     if (!c->kp.dbg_ts) return fail(SK_ESTATE, "set SHIFTK_DEBUG_TS before sk_init");
+    CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(out16, c->kp.dbg_ts, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return SK_OK;
@@ -1063,6 +1069,9 @@ int sk_apply_operator(const sk_operator *H, const sk_cplx *r, sk_cplx *q, void *
     } else if (H->kind == SK_OP_HEISENBERG_SZ) {
         if (H->L < 1 || H->L > 34 || H->n_up < 0 || H->n_up > H->L || H->M < 1)
             return fail(SK_EINVAL, "L/n_up/M");
+        int64_t dim = 1;   // C(L, n_up): the kernel writes every sector row, so M must be it
+        for (int j = 1; j <= H->n_up; ++j) dim = dim * (H->L - H->n_up + j) / j;
+        if (H->M != dim) return fail(SK_EINVAL, "Heisenberg sector: need M = C(L, n_up)");
         a.M = H->M;
         CK(sk::launch_heisenberg_sz(a, KParams{}, H->L, H->n_up, H->J, s));
     } else if (H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) {

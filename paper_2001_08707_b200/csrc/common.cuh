@@ -154,6 +154,14 @@ struct KParams {
     int32_t defer;
     int32_t wred_n;
     int64_t wred_off, wred_stride;
+    // bond split (one GPU, Heisenberg chain, COCG, N_left = 1): the SpMV applies
+    // H_A (diagonal + bonds i < split_ahi), the update H_B (the other bonds) in its own row order
+    // and the partials of w_B = <r, H_B r> of the r it writes, at [wsplit_off, + nblk_upd) of
+    // the next half of part_w (inside the range the seed step reduces).  split_ahi = 0: off.
+    int32_t split_ahi;
+    int32_t pad_split_;
+    int64_t wsplit_off;
+    double J;                    // exchange coupling of the Heisenberg operator (H_B amplitudes)
     // per-shift arrays [nz]
     const cplx *z;
     cplx *pibuf;         // [3][nz] rotating pi_n^k

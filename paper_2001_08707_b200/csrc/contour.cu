@@ -112,7 +112,7 @@ int sk_combine(const sk_cplx *X, int64_t n_in, int64_t ld_x, int64_t M, const sk
     if (cudaMemcpyAsync(Wd, W, wb, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return sk_set_error(SK_ECUDA, "sk_combine: W copy");
     int64_t g = (M + sk::kThreads - 1) / sk::kThreads;
-    if (g > 4 * 148) g = 4 * 148;
+    if (g > 4 * sk::sm_count()) g = 4 * sk::sm_count();
     for (int c0 = 0; c0 < n_out; c0 += sk::kCombineOut) {
         const int nc = (int)(n_out - c0 < sk::kCombineOut ? n_out - c0 : sk::kCombineOut);
         sk::combine_kernel<<<(int)g, sk::kThreads, 0, s>>>((const cplx *)X, n_in, ld_x, M, Wd, (int)n_out, c0, nc,
@@ -130,18 +130,18 @@ int sk_gram(const sk_cplx *A, int64_t na, const sk_cplx *B, int64_t nb, int64_t 
     cudaStream_t s = (cudaStream_t)stream;
     const int np = (int)(na * nb);
     int64_t g = (M + sk::kGramRows - 1) / sk::kGramRows;
-    if (g > 2 * 148) g = 2 * 148;
+    if (g > 2 * sk::sm_count()) g = 2 * sk::sm_count();
     cplx *part = nullptr, *Gd = nullptr;
     if (cudaMallocAsync((void **)&part, sizeof(cplx) * (size_t)g * np, s) != cudaSuccess ||
         cudaMallocAsync((void **)&Gd, sizeof(cplx) * (size_t)np, s) != cudaSuccess)
         return sk_set_error(SK_ECUDA, "sk_gram: scratch");
     const size_t shm = sizeof(cplx) * (size_t)(na + nb) * sk::kGramRows;
-    static bool cfg = false;
-    if (!cfg) {
-        cudaFuncSetAttribute(sk::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(cplx) * 2 * sk::kGramMax * sk::kGramRows));
-        cfg = true;
-    }
+    static sk::PerDevice cfg;
+    if (sk::once_per_device(cfg, [] {
+            return cudaFuncSetAttribute(sk::gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(cplx) * 2 * sk::kGramMax * sk::kGramRows));
+        }) != cudaSuccess)
+        return sk_set_error(SK_ECUDA, "sk_gram: shared-memory attribute");
     sk::gram_kernel<<<(int)g, sk::kThreads, shm, s>>>((const cplx *)A, (int)na, (const cplx *)B, (int)nb, M, part);
     sk::gram_reduce_kernel<<<(np + 255) / 256, 256, 0, s>>>(part, (int)g, np, Gd);
     const cudaError_t e1 = cudaMemcpyAsync(G, Gd, sizeof(cplx) * (size_t)np, cudaMemcpyDeviceToHost, s);

@@ -1,5 +1,6 @@
 // kernels.cuh — launch wrappers of the hot-path kernels (spmv.cu, update.cu, scalar.cu).
 #pragma once
+#include <mutex>
 #include <utility>
 
 #include "common.cuh"
@@ -28,10 +29,31 @@ cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int block, size_t smem,
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Per-device one-time setup (cudaFuncSetAttribute, __device__ tables): both are per device, so a
+// process that drives several GPUs must run it on each — keyed by the current device.
+struct PerDevice {
+    std::mutex mu;
+    uint64_t done = 0;   // bit d: done on device d (d < 64)
+};
+template <typename F>
+cudaError_t once_per_device(PerDevice &pd, F &&f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(pd.mu);
+    if ((pd.done >> dev) & 1ull) return cudaSuccess;
+    e = f();
+    if (e == cudaSuccess) pd.done |= 1ull << dev;
+    return e;
+}
+
 constexpr int kThreads = 256;          // streaming kernels
 constexpr int kScalarThreads = 1024;   // the single-CTA init / finish kernel
-constexpr int kMaxBlocks = 148 * 8;    // grid cap for grid-stride streaming kernels
-constexpr int kMaxSpmvBlocks = 148 * 32;   // grid cap (= partial slots) of the SpMV kernels
+// partial-slot capacities (arena sizes); grids are sized from sm_count() and capped by these
+constexpr int kMaxSms = 192;
+constexpr int kMaxBlocks = kMaxSms * 8;      // grid cap for grid-stride streaming kernels
+constexpr int kMaxSpmvBlocks = kMaxSms * 32; // grid cap (= partial slots) of the SpMV kernels
 // w = <r, q> is reduced in a fixed order whatever CTA takes a tile: one partial per tile; up to
 // kStreamDirect tiles the seed CTA sums them all, beyond that the CTA completing a group of
 // kStreamGroup tiles sums the group (partials [ntiles, ntiles + ngroups) of part_w).
@@ -48,7 +70,7 @@ int sz_blocks(int L, int64_t M, int bicg);
 int64_t sz_partials(int L);                          // w partials of the sector SpMV (0: per CTA)                     // worker CTAs of the sector SpMV
 bool heis_stream(int L, int64_t M, int bicg);      // the TMA-fed streaming kernel is used
 bool heis_pairs(int L, int64_t M);                 // ... as tile pairs across the top spin bit (one GPU)
-int sm_count();
+int sm_count();                                  // SMs of the current device
 int csr_blocks(int64_t M);                      // worker CTAs (= partials) of the CSR SpMV
 int update_blocks(int64_t M, int nl, int full, int nz); // worker CTAs (= partials) of the update
 int shift_agents(int nz);                        // shift-agent CTAs of the update

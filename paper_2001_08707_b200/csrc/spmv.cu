@@ -26,19 +26,21 @@ bool pdl_enabled() {
 
 int stream_blocks(int64_t M) {
     int64_t b = (M + kThreads - 1) / kThreads;
-    if (b > kMaxBlocks) b = kMaxBlocks;
+    if (b > 8 * (int64_t)sm_count()) b = 8 * (int64_t)sm_count();
     if (b < 1) b = 1;
     return (int)b;
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+int sm_count() {   // per device (cached): grids are sized for the device the launch goes to
+    static int n[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!n[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        n[dev] = v > kMaxSms ? kMaxSms : v;
     }
-    return n;
+    return n[dev];
 }
 
 // The streaming (TMA-fed) kernel wins once the vector outgrows L2 (measured: L=24 215 vs 233 us,

@@ -56,7 +56,11 @@ static __device__ __forceinline__ U tile_bonds(U base) {
     return (tbits ^ (tbits >> 1)) & ((((U)1) << (L - 1 - T)) - (U)1);
 }
 
-template <int L, int T, bool MULTI>
+// SPLIT (one GPU, COCG, projection mode): this kernel applies only H_A — the
+// diagonal and the bonds (i, i+1) with i < kp.split_ahi (the arc kept local by the tile + the L2
+// window) — and leaves H_B (bonds i >= split_ahi and the periodic bond) to the update kernel,
+// which applies it from shared memory in its own row order (update_split.cu).
+template <int L, int T, bool MULTI, bool SPLIT = false>
 __global__ void __launch_bounds__(kStreamThreads, 2)
 heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
     constexpr int TS = 1 << T;
@@ -80,6 +84,8 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
     const int64_t ntiles = a.M >> T;
     const U row0 = (U)(MULTI ? rv.row0 : 0);
     cplx *const pw = (a.part_w && a.st && kp.defer) ? a.part_w + (a.st->seq & 1) * kp.wred_stride : a.part_w;
+    // tile-level bonds applied here: all, or (SPLIT) those with i < split_ahi (bit j = bond j + T)
+    const U amask = SPLIT ? (U)((((U)1) << (kp.split_ahi - T)) - (U)1) : ~(U)0;
     cplx w = mk(0.0, 0.0);
     if (!agent) {
         if (tid == 0) {
@@ -117,8 +123,9 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
                     }
                     // partner items, in the consumers' order
                     const U tb = (base >> T) & (U)1;
-                    U act = tile_bonds<L, T, U>(base);
+                    U act = tile_bonds<L, T, U>(base) & amask;
                     for (int m = -2;; ++m) {
+                        if (SPLIT && m == -1) continue;   // the periodic bond is in H_B
                         const cplx *src;
                         unsigned bytes = TS * sizeof(cplx);
                         if (m == -2) {          // bond (T-1, T): the half with bit T-1 = tb
@@ -169,8 +176,9 @@ heisenberg_stream_kernel(SpmvArgs a, KParams kp, double J) {
                     v0[e] = ot[ls];
                     q[e] = mk(d * v0[e].x, d * v0[e].y);
                 }
-                U act = tile_bonds<L, T, U>(base);
+                U act = tile_bonds<L, T, U>(base) & amask;
                 for (int m = -2;; ++m) {
+                    if (SPLIT && m == -1) continue;
                     if (m >= 0) {
                         if (!act) break;
                         act &= act - (U)1;
@@ -554,14 +562,18 @@ template <int L>
 static cudaError_t launch_stream(const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s) {
     constexpr int T = kTileBits;
     const size_t shm = (size_t)(2 + kStreamSlots) * sizeof(cplx) << T;
-    static bool cfg = false;
-    if (!cfg) {
-        cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-        cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-        cudaFuncSetAttribute(heisenberg_pair_kernel<L, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-        cfg = true;
-    }
+    static PerDevice cfg;
+    cudaError_t e = once_per_device(cfg, [&] {
+        cudaError_t r = cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(heisenberg_pair_kernel<L, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(heisenberg_stream_kernel<L, T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        return r;
+    });
+    if (e != cudaSuccess) return e;
     const bool p = a.st != nullptr;
+    if (kp.split_ahi > 0 && a.st)   // solver mode with the bond split: H_A only
+        return launch_k(heisenberg_stream_kernel<L, T, false, true>, grid, kStreamThreads, shm, s, p, a, kp, J);
     if (kp.world > 1)
         return launch_k(heisenberg_stream_kernel<L, T, true>, grid, kStreamThreads, shm, s, p, a, kp, J);
     if (heis_pairs(L, a.M))

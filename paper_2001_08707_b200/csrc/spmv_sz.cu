@@ -397,10 +397,11 @@ __global__ void __launch_bounds__(kThreads, NRHS == 2 ? SZB_MINB - 1 : SZB_MINB)
 }
 
 
+// g_sz_tab is a __device__ symbol: one copy per device, so it is written on every device a
+// sector operator runs on (once each).
 static cudaError_t sz_tables_init() {
-    static std::once_flag once;
-    static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
+    static PerDevice once;
+    return once_per_device(once, [] {
         static SzTables h;
         for (int n = 0; n <= kSzMaxL; ++n)
             for (int k = 0; k <= kSzMaxL; ++k)
@@ -416,9 +417,8 @@ static cudaError_t sz_tables_init() {
                 }
         }
         h.lo_off[kSzLoBits + 1] = pos;
-        err = cudaMemcpyToSymbol(g_sz_tab, &h, sizeof(h));
+        return cudaMemcpyToSymbol(g_sz_tab, &h, sizeof(h));
     });
-    return err;
 }
 
 // SHIFTK_SZ_RANK=1 selects the rank-stepping kernel (kept for comparison)

@@ -220,14 +220,16 @@ static cudaError_t launch_tiled(const SpmvArgs &a, const KParams &kp, double J, 
     const size_t shm = sizeof(cplx) << T;
     const bool p = a.st != nullptr;
     if (a.bicg) {
-        static bool cfg = false;
-        if (!cfg) {
-            cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
-            cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
-            cfg = true;
-        }
+        static PerDevice cfg;
+        const cudaError_t e = once_per_device(cfg, [&] {
+            cudaError_t r = cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2, false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
+            if (r == cudaSuccess)
+                r = cudaFuncSetAttribute(heisenberg_tiled_kernel<L, T, 2, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * shm));
+            return r;
+        });
+        if (e != cudaSuccess) return e;
         if (kp.world > 1)
             return launch_k(heisenberg_tiled_kernel<L, T, 2, true>, grid, kThreads, 2 * shm, s, p, a, kp, J);
         return launch_k(heisenberg_tiled_kernel<L, T, 2, false>, grid, kThreads, 2 * shm, s, p, a, kp, J);

@@ -247,7 +247,10 @@ static __device__ void finish_step(const KParams &kp, StepScratch &sc, bool eage
         const cplx f = best.f, fp = best.fp;
         const int bst = best.idx;
         double rmin;
-        const bool all_retire = retire_test(nu, f, S->tol, rmin);
+        // (bst < 0: no agent kept a survivor — possible only when the lazy test of the agents and
+        // this one differ by an ulp at res == tol; nothing is left to switch to, so it is the
+        // all-retire case: retire_pass below makes it CONVERGED)
+        const bool all_retire = bst < 0 || retire_test(nu, f, S->tol, rmin);
         const bool sw = !all_retire && !(kp.flags & 1) && bst != S->seed;
         cplx rf = mk(1, 0);
         if (sw) {   // a9 / R9: the new seed's r, r_prev, pi, alpha, rho in its own normalisation

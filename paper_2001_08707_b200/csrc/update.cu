@@ -22,7 +22,7 @@ int shift_agents(int nz) {
 int update_blocks(int64_t M, int nl, int full, int nz) {
     const int R = 1;   // rows per thread per chunk (the non-full kernel pipelines two chunks)
     int64_t b = (M + (int64_t)kThreads * R - 1) / ((int64_t)kThreads * R);
-    const int64_t cap = 148 * UPD_MINB - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
+    const int64_t cap = (int64_t)sm_count() * UPD_MINB - shift_agents(nz);   // + the agents = one full wave at 4 CTAs/SM
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;

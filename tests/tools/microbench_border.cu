@@ -1,0 +1,281 @@
+// Memory-pattern prototype of the split-bond update: does an update that walks
+// the rows in "B order" — tiles made of 2^PB-state pieces (16·2^PB B contiguous) taken at every
+// combination of the HB top spin bits (pieces 2^AHI states apart) — stream r_n, q, r_{n-1}, b
+// and write r_{n+1} as fast as the linear update?  Each B-tile is staged in shared memory and
+// the off-diagonal bonds among its bits are applied twice (to r_n and to r_{n+1}), as the real
+// kernel does.  Prints GB/s of the 80 algorithmic bytes per row.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mbb microbench_border.cu && /tmp/mbb
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef double2 cplx;
+__device__ __forceinline__ cplx ldcs(const cplx *p) { return __ldcs(p); }
+
+__global__ void lin(const cplx *__restrict__ rc, const cplx *__restrict__ rp, const cplx *__restrict__ q,
+                    const cplx *__restrict__ b, cplx *__restrict__ rn, int64_t M, double2 *part) {
+    double ax = 0, ay = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        cplx a = ldcs(rc + i), c = ldcs(rp + i), d = ldcs(q + i), e = ldcs(b + i);
+        cplx o = make_double2(0.5 * a.x + 0.25 * d.x - 0.125 * c.x, 0.5 * a.y + 0.25 * d.y - 0.125 * c.y);
+        __stcs(rn + i, o);
+        ax += o.x * e.x;
+        ay += o.y * e.y;
+    }
+    if (ax == 1234.5) part[0] = make_double2(ax, ay);
+}
+
+template <int L, int AHI, int PB, int NT>
+__global__ void __launch_bounds__(NT, 1) bord(const cplx *__restrict__ rc, const cplx *__restrict__ rp,
+                                              const cplx *__restrict__ q, const cplx *__restrict__ b,
+                                              cplx *__restrict__ rn, double2 *part, unsigned long long *work,
+                                              int dyn) {
+    constexpr int HB = L - AHI, TB = PB + HB, TS = 1 << TB, PER = TS / NT;
+    static_assert(PER * NT == TS, "");
+    extern __shared__ cplx S[];
+    __shared__ int64_t tnext;
+    const int64_t ntiles = int64_t(1) << (AHI - PB);
+    const int tid = threadIdx.x;
+    double wx = 0, wy = 0, ax = 0;
+    int64_t t = dyn ? 0 : blockIdx.x;
+    if (dyn) {
+        if (tid == 0) tnext = (int64_t)atomicAdd(work, 1ull);
+        __syncthreads();
+        t = tnext;
+    }
+    while (t < ntiles) {
+        cplx v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            const int64_t s = ((int64_t)(e >> PB) << AHI) | (t << PB) | (e & ((1 << PB) - 1));
+            v[k] = ldcs(rc + s);
+            S[e] = v[k];
+        }
+        __syncthreads();
+        if (dyn && tid == 0) tnext = (int64_t)atomicAdd(work, 1ull);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            const int64_t s = ((int64_t)(e >> PB) << AHI) | (t << PB) | (e & ((1 << PB) - 1));
+            cplx h = ldcs(q + s);
+            const cplx c = ldcs(rp + s), d = ldcs(b + s);
+#pragma unroll
+            for (int j = 0; j < HB - 1; ++j)
+                if (((e >> (PB + j)) ^ (e >> (PB + j + 1))) & 1) {
+                    const cplx p = S[e ^ (3 << (PB + j))];
+                    h.x += 0.5 * p.x;
+                    h.y += 0.5 * p.y;
+                }
+            if (((e >> (TB - 1)) ^ e) & 1) {
+                const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
+                h.x += 0.5 * p.x;
+                h.y += 0.5 * p.y;
+            }
+            const cplx o = make_double2(0.5 * v[k].x + 0.25 * h.x - 0.125 * c.x, 0.5 * v[k].y + 0.25 * h.y - 0.125 * c.y);
+            __stcs(rn + s, o);
+            ax += o.x * d.x + o.y * d.y;
+            v[k] = o;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) S[tid + k * NT] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            cplx h = make_double2(0, 0);
+#pragma unroll
+            for (int j = 0; j < HB - 1; ++j)
+                if (((e >> (PB + j)) ^ (e >> (PB + j + 1))) & 1) {
+                    const cplx p = S[e ^ (3 << (PB + j))];
+                    h.x += p.x;
+                    h.y += p.y;
+                }
+            if (((e >> (TB - 1)) ^ e) & 1) {
+                const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
+                h.x += p.x;
+                h.y += p.y;
+            }
+            wx += v[k].x * h.x - v[k].y * h.y;
+            wy += v[k].x * h.y + v[k].y * h.x;
+        }
+        if (dyn) {
+            __syncthreads();
+            t = tnext;
+        } else {
+            __syncthreads();
+            t += gridDim.x;
+        }
+    }
+    if (wx + ax == 1234.5) part[0] = make_double2(wx, wy);
+}
+
+// Variant: r_n tiles staged with cp.async (16 B per thread-row, no registers held), double
+// buffered so tile t+1's r_n is in flight while tile t is computed; r_{n+1} written in place.
+__device__ __forceinline__ void cpa16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+template <int L, int AHI, int PB, int NT>
+__global__ void __launch_bounds__(NT, 1) bord2(const cplx *__restrict__ rc, const cplx *__restrict__ rp,
+                                               const cplx *__restrict__ q, const cplx *__restrict__ b,
+                                               cplx *__restrict__ rn, double2 *part) {
+    constexpr int HB = L - AHI, TB = PB + HB, TS = 1 << TB, PER = TS / NT;
+    static_assert(PER * NT == TS, "");
+    extern __shared__ cplx S2[];   // [2][TS]
+    const int64_t ntiles = int64_t(1) << (AHI - PB);
+    const int tid = threadIdx.x;
+    double wx = 0, wy = 0, ax = 0;
+    auto row = [&](int64_t t, int e) { return ((int64_t)(e >> PB) << AHI) | (t << PB) | (e & ((1 << PB) - 1)); };
+    int64_t t = blockIdx.x;
+    if (t < ntiles)
+        for (int k = 0; k < PER; ++k) cpa16(S2 + tid + k * NT, rc + row(t, tid + k * NT));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
+        cplx *S = S2 + (it & 1) * TS;
+        const int64_t tn = t + gridDim.x;
+        if (tn < ntiles)
+            for (int k = 0; k < PER; ++k) cpa16(S2 + ((it + 1) & 1) * TS + tid + k * NT, rc + row(tn, tid + k * NT));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        cplx o[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            const int64_t s = row(t, e);
+            cplx h = ldcs(q + s);
+            const cplx c = ldcs(rp + s), d = ldcs(b + s);
+            const cplx v = S[e];
+#pragma unroll
+            for (int j = 0; j < HB - 1; ++j)
+                if (((e >> (PB + j)) ^ (e >> (PB + j + 1))) & 1) {
+                    const cplx p = S[e ^ (3 << (PB + j))];
+                    h.x += 0.5 * p.x;
+                    h.y += 0.5 * p.y;
+                }
+            if (((e >> (TB - 1)) ^ e) & 1) {
+                const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
+                h.x += 0.5 * p.x;
+                h.y += 0.5 * p.y;
+            }
+            o[k] = make_double2(0.5 * v.x + 0.25 * h.x - 0.125 * c.x, 0.5 * v.y + 0.25 * h.y - 0.125 * c.y);
+            __stcs(rn + s, o[k]);
+            ax += o[k].x * d.x + o[k].y * d.y;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) S[tid + k * NT] = o[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = tid + k * NT;
+            cplx h = make_double2(0, 0);
+#pragma unroll
+            for (int j = 0; j < HB - 1; ++j)
+                if (((e >> (PB + j)) ^ (e >> (PB + j + 1))) & 1) {
+                    const cplx p = S[e ^ (3 << (PB + j))];
+                    h.x += p.x;
+                    h.y += p.y;
+                }
+            if (((e >> (TB - 1)) ^ e) & 1) {
+                const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
+                h.x += p.x;
+                h.y += p.y;
+            }
+            wx += o[k].x * h.x - o[k].y * h.y;
+            wy += o[k].x * h.y + o[k].y * h.x;
+        }
+        __syncthreads();   // S (this buffer) is refilled two tiles later
+    }
+    if (wx + ax == 1234.5) part[0] = make_double2(wx, wy);
+}
+
+static float timeit(void (*f)(void *), void *arg, int reps) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    f(arg);
+    cudaEventRecord(a);
+    for (int i = 0; i < reps; ++i) f(arg);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms / reps;
+}
+
+struct Bufs {
+    cplx *v[5];
+    double2 *part;
+    unsigned long long *work;
+    int64_t M;
+    int grid, dyn;
+};
+static Bufs G;
+
+static void run_lin(void *) { lin<<<148 * 8, 256>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.M, G.part); }
+template <int L, int AHI, int PB, int NT>
+static void run_b(void *) {
+    constexpr int TS = 1 << (PB + L - AHI);
+    cudaMemsetAsync(G.work, 0, 8);
+    bord<L, AHI, PB, NT><<<G.grid, NT, TS * sizeof(cplx)>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.part, G.work, G.dyn);
+}
+template <int L, int AHI, int PB, int NT>
+static void bench(int ctas) {
+    constexpr int TS = 1 << (PB + L - AHI);
+    cudaFuncSetAttribute(bord<L, AHI, PB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS * (int)sizeof(cplx));
+    for (int dyn = 0; dyn < 2; ++dyn) {
+        G.grid = 148 * ctas;
+        G.dyn = dyn;
+        float ms = timeit(run_b<L, AHI, PB, NT>, nullptr, 3);
+        cudaError_t e = cudaGetLastError();
+        printf("B-order L=%d AHI=%d PB=%d (piece %4d B, tile %3d KB) NT=%4d ctas/SM=%d %s: %8.3f ms  %7.1f GB/s  %s\n", L, AHI, PB,
+               16 << PB, TS * 16 / 1024, NT, ctas, dyn ? "queue " : "static", ms, 80.0 * G.M / (ms * 1e6),
+               cudaGetErrorString(e));
+    }
+}
+
+template <int L, int AHI, int PB, int NT>
+static void run_b2(void *) {
+    constexpr int TS = 1 << (PB + L - AHI);
+    bord2<L, AHI, PB, NT><<<G.grid, NT, 2 * TS * sizeof(cplx)>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.part);
+}
+template <int L, int AHI, int PB, int NT>
+static void bench2(int ctas) {
+    constexpr int TS = 1 << (PB + L - AHI);
+    cudaFuncSetAttribute(bord2<L, AHI, PB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TS * (int)sizeof(cplx));
+    G.grid = 148 * ctas;
+    float ms = timeit(run_b2<L, AHI, PB, NT>, nullptr, 3);
+    cudaError_t e = cudaGetLastError();
+    printf("B-order/cp.async x2 L=%d AHI=%d PB=%d (piece %4d B, tile %3d KB) NT=%4d ctas/SM=%d: %8.3f ms  %7.1f GB/s  %s\n", L, AHI, PB,
+           16 << PB, TS * 16 / 1024, NT, ctas, ms, 80.0 * G.M / (ms * 1e6), cudaGetErrorString(e));
+}
+
+int main() {
+    G.M = int64_t(1) << 30;
+    for (int i = 0; i < 5; ++i) {
+        if (cudaMalloc(&G.v[i], G.M * sizeof(cplx)) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+        cudaMemset(G.v[i], 0, G.M * sizeof(cplx));
+    }
+    cudaMalloc(&G.part, 64);
+    cudaMalloc(&G.work, 64);
+    float ms = timeit(run_lin, nullptr, 3);
+    printf("linear update                      : %8.3f ms  %7.1f GB/s\n", ms, 80.0 * G.M / (ms * 1e6));
+    bench<30, 21, 4, 1024>(1);
+    bench<30, 21, 4, 512>(1);
+    bench<30, 21, 3, 512>(2);
+    bench<30, 21, 3, 256>(3);
+    bench<30, 22, 4, 512>(2);
+    bench<30, 21, 5, 1024>(1);   // 256 KB: does not fit (expect an error)
+    bench<30, 20, 3, 1024>(1);
+    bench<30, 19, 2, 1024>(1);
+    bench2<30, 21, 3, 512>(1);
+    bench2<30, 21, 3, 1024>(1);
+    bench2<30, 22, 4, 512>(1);
+    bench2<30, 22, 4, 1024>(1);
+    bench2<30, 21, 2, 512>(2);
+    bench2<30, 22, 3, 512>(2);
+    bench2<30, 23, 4, 512>(2);
+    return 0;
+}
