@@ -270,6 +270,19 @@ int sk_profile_enable(sk_ctx *ctx, int32_t on);
 /* Synchronises the stream, accumulates the recorded events into *out; reset != 0 clears. */
 int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
 
+/* The execution plan sk_init chose for a context (diagnostics; bench.py reports it).
+   split_ahi > 0: the Heisenberg bond split — the SpMV applies the diagonal and
+   the bonds (i, i+1), i < split_ahi; the update kernel applies the bonds i >= split_ahi and the
+   periodic bond in its B-tile row order; 0: one kernel applies the whole operator. */
+typedef struct {
+    int32_t split_ahi;       /* see above                                                      */
+    int32_t spmv_ctas;       /* worker CTAs (= w partials) of the SpMV                         */
+    int32_t update_ctas;     /* streaming CTAs of the update kernel                            */
+    int32_t shift_agents;    /* shift-agent CTAs of the update kernel                          */
+    int64_t arena_bytes;     /* device bytes the context owns                                  */
+} sk_info;
+int sk_get_info(sk_ctx *ctx, sk_info *out);
+
 /* Diagnostics: %globaltimer stamps (ns) written by instrumented kernels (16 slots; see
    csrc/steps.cuh).  Requires the environment variable SHIFTK_DEBUG_TS at sk_init. */
 int sk_debug_timestamps(sk_ctx *ctx, int64_t *out16);

@@ -384,10 +384,13 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     kp.full = c->full;
     kp.a_is_b = c->a_is_b;
     kp.flags = c->flags;
-    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M, kp.bicg)
+    kp.J = H->J;
+    kp.split_ahi = sk::split_ahi_for(H->L, M, world, kp.bicg, c->full, c->nl, H->kind == SK_OP_HEISENBERG);
+    kp.nblk_spmv = H->kind == SK_OP_HEISENBERG ? sk::heisenberg_blocks(H->L, M, kp.bicg, kp.split_ahi > 0)
                    : H->kind == SK_OP_HEISENBERG_SZ ? sk::sz_blocks(H->L, M, kp.bicg)
                    : H->kind == SK_OP_RC ? sk::stream_blocks(M) : sk::csr_blocks(M);
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
+    if (kp.split_ahi) kp.nblk_upd = sk::split_blocks();
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
     kp.rank = rank;
@@ -417,7 +420,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
             // the w partials the seed step reduces: [wred_off, wred_off + wred_n) of a half
             kp.wred_off = 0;
             kp.wred_n = kp.nblk_spmv;
-            if (H->kind == SK_OP_HEISENBERG && sk::heis_stream(H->L, M, kp.bicg)) {
+            if (H->kind == SK_OP_HEISENBERG && sk::heis_stream(H->L, M, kp.bicg, kp.split_ahi > 0)) {
                 const int64_t nt = M >> sk::kTileBits;
                 np = std::max<int64_t>(np, sk::stream_partials(nt));
                 ng = std::max<int64_t>(1, (nt + sk::kStreamGroup - 1) / sk::kStreamGroup);
@@ -434,6 +437,12 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
             // deferred seed step on one GPU with the built-in operator: two halves (iteration
             // parity), because the next SpMV writes its partials while the finish reads these
             kp.defer = (world == 1 && H->kind != SK_OP_RC) ? 1 : 0;
+            if (kp.split_ahi) {   // the update's w_B partials follow the SpMV's (same reduced range;
+                                  // per-tile/group partials of the streaming kernel, else per CTA)
+                kp.wsplit_off = kp.wred_off + kp.wred_n;
+                kp.wred_n += kp.nblk_upd;
+                np = std::max<int64_t>(np, kp.wsplit_off + kp.nblk_upd);
+            }
             kp.wred_stride = np;
             add(&kp.part_w, sizeof(cplx) * np * 2);
             add(&kp.grp, sizeof(uint32_t) * ng);
@@ -526,6 +535,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         if (cudaStreamSynchronize(c->stream)) return bail(fail(SK_ECUDA, "sync"));
     }
     if (sk::launch_init(kp, c->b, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init kernel"));
+    if (kp.split_ahi && sk::launch_split_init(kp, c->stream) != cudaSuccess)
+        return bail(fail(SK_ECUDA, "split init kernel"));
     if (world > 1) {   // the global rho_0, ||b||, P b need the other ranks: finished at connect
         if (sk::launch_reduce_local(kp, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init reduce"));
         if (group) group->members[rank] = c;
@@ -791,6 +802,8 @@ int sk_update(sk_ctx *c, int32_t *status) {
 int sk_update_rc(sk_ctx *c, const sk_cplx *q, const sk_cplx *qt, int32_t *status) {
     if (!c) return fail(SK_ESTATE, "null context");
     if (!q || (c->method == SK_BICG && !qt)) return fail(SK_EINVAL, "q (and qt for BiCG) required");
+    if (c->kp.split_ahi)   // its update adds H_B r itself (the library's own operator)
+        return fail(SK_EUNSUPPORTED, "sk_update_rc on a bond-split Heisenberg context (SHIFTK_HEIS_SPLIT=0 disables the split)");
     CK(cudaSetDevice(c->device));
     int rc;
     if ((rc = enqueue_finish(c)) != SK_OK) return rc;
@@ -1021,6 +1034,16 @@ int sk_get_profile(sk_ctx *c, sk_profile *o, int32_t reset) {
         c->prof_iters = 0;
         c->prof_ms[0] = c->prof_ms[1] = c->prof_ms[2] = 0;
     }
+    return SK_OK;
+}
+
+int sk_get_info(sk_ctx *c, sk_info *o) {
+    if (!c || !o) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    o->split_ahi = c->kp.split_ahi;
+    o->spmv_ctas = c->kp.nblk_spmv;
+    o->update_ctas = c->kp.nblk_upd;
+    o->shift_agents = c->kp.n_agents;
+    o->arena_bytes = (int64_t)c->arena_bytes;
     return SK_OK;
 }
 

@@ -65,10 +65,11 @@ inline __host__ __device__ int64_t stream_partials(int64_t ntiles) {
 constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
 
 int stream_blocks(int64_t M);
-int heisenberg_blocks(int L, int64_t M, int bicg);   // worker CTAs (= partials) of the Heisenberg SpMV
+// worker CTAs (= partials) of the Heisenberg SpMV; split: the SpMV of a bond-split solver (H_A)
+int heisenberg_blocks(int L, int64_t M, int bicg, bool split = false);
 int sz_blocks(int L, int64_t M, int bicg);
 int64_t sz_partials(int L);                          // w partials of the sector SpMV (0: per CTA)                     // worker CTAs of the sector SpMV
-bool heis_stream(int L, int64_t M, int bicg);      // the TMA-fed streaming kernel is used
+bool heis_stream(int L, int64_t M, int bicg, bool split = false);   // the TMA-fed streaming kernel is used
 bool heis_pairs(int L, int64_t M);                 // ... as tile pairs across the top spin bit (one GPU)
 int sm_count();                                  // SMs of the current device
 int csr_blocks(int64_t M);                      // worker CTAs (= partials) of the CSR SpMV
@@ -107,6 +108,14 @@ cudaError_t launch_init(const KParams &kp, const cplx *b, cudaStream_t s);
 // Fused three-term update (+ shadow) + next-iteration dots + (full mode) all-shift x/p update;
 // CTA 0 runs the per-shift recurrences.
 cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s);
+
+// Bond split (update_split.cu): AHI = L - 8 when the split applies to this
+// context (one GPU, Heisenberg chain, COCG, N_left = 1, streaming SpMV), else 0; the update then
+// applies H_B and writes the w_B partials; launch_split_init writes those of r_0.
+int split_ahi_for(int L, int64_t M, int world, int bicg, int full, int nl, int kind_heisenberg);
+int split_blocks();
+cudaError_t launch_update_split(const KParams &kp, const cplx *q, cudaStream_t s);
+cudaError_t launch_split_init(const KParams &kp, cudaStream_t s);
 
 // Single-CTA steps outside the iteration: INIT (after launch_init) and FINISH (residuals,
 // retirement, switch of a pending iteration).

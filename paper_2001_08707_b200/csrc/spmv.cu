@@ -46,13 +46,20 @@ int sm_count() {   // per device (cached): grids are sized for the device the la
 // The streaming (TMA-fed) kernel wins once the vector outgrows L2 (measured: L=24 215 vs 233 us,
 // L=26 0.98 vs 1.25 ms, L=28 4.8 vs 6.8 ms); below that the tiled kernel's shorter per-tile
 // latency chain wins (L=20 13.4 vs 14.6 us).  SHIFTK_HEIS_STREAM=0/1 forces either.
-bool heis_stream(int L, int64_t M, int bicg) {
+static int stream_env() {
     static int en = -2;
     if (en == -2) {
         const char *e = getenv("SHIFTK_HEIS_STREAM");
         en = !e ? -1 : (e[0] == '0' ? 0 : 1);
     }
+    return en;
+}
+bool heis_stream(int L, int64_t M, int bicg, bool split) {
+    const int en = stream_env();
     if (en == 0 || bicg || L <= kTileBits || L > 34 || M < (int64_t(1) << kTileBits)) return false;
+    // H_A of the bond split reaches only L2-resident partner tiles: there the
+    // tiled kernel's direct loads win (L=30: 11.7 vs 16.3 ms); SHIFTK_HEIS_STREAM=1 forces it
+    if (split) return en == 1;
     return en == 1 || (M >> kTileBits) >= 8192;
 }
 
@@ -67,8 +74,8 @@ bool heis_pairs(int L, int64_t M) {
     return en && L >= 24 && M == (int64_t(1) << L);
 }
 
-int heisenberg_blocks(int L, int64_t M, int bicg) {
-    if (heis_stream(L, M, bicg)) {   // two CTAs per SM, one slot left for the finish agent
+int heisenberg_blocks(int L, int64_t M, int bicg, bool split) {
+    if (heis_stream(L, M, bicg, split)) {   // two CTAs per SM, one slot left for the finish agent
         const int64_t ntiles = M >> kTileBits, slots = 2 * (int64_t)sm_count() - 1;
         return (int)(ntiles < slots ? ntiles : slots);
     }
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) heisenberg_kernel(SpmvArgs a, KParam
 }
 
 cudaError_t launch_heisenberg(const SpmvArgs &a, const KParams &kp, int L, double J, cudaStream_t s) {
-    const int workers = heisenberg_blocks(L, a.M, a.bicg);
+    const int workers = heisenberg_blocks(L, a.M, a.bicg, kp.split_ahi > 0 && a.st);
     const int grid = workers + (a.st ? 1 : 0);
     if (a.M >= (int64_t(1) << kTileBits) && L > kTileBits && L <= 34) {
         if (L <= 16) return launch_tiled_a(L, a, kp, J, grid, s);

@@ -14,7 +14,10 @@ namespace sk {
 //            whole tile takes part or none: the active set is uniform per CTA), three partner
 //            tiles per round, each a coalesced stream;
 //   then the T-1 bonds inside the tile from shared memory.
-template <int L, int T, int NRHS, bool MULTI>
+// SPLIT (one GPU, COCG, N_left = 1): only H_A — the diagonal and the bonds
+// (i, i+1), i < kp.split_ahi; the periodic bond and the bonds i >= split_ahi are applied by the
+// update kernel (update_split.cu).
+template <int L, int T, int NRHS, bool MULTI, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads, NRHS == 1 ? 4 : 2)
 heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
     extern __shared__ cplx tile[];   // [NRHS][2^T]
@@ -61,7 +64,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 const int l1 = ls ^ (1 << (T - 1));
                 v1[k] = on1 ? p1[l1] : mk(0.0, 0.0);
                 if (NRHS == 2) t1[k] = on1 ? p1t[l1] : mk(0.0, 0.0);
-                const bool on2 = ((U)(ls & 1) ^ hb) != 0;                 // bond (L-1, 0)
+                const bool on2 = !SPLIT && ((U)(ls & 1) ^ hb) != 0;      // bond (L-1, 0)
                 v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
                 if (NRHS == 2) t2[k] = on2 ? p2t[ls ^ 1] : mk(0.0, 0.0);
             }
@@ -85,6 +88,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
         if (L - 1 > T) {
             const U tbits = base >> T;   // bit (i - T) of tbits = site i, for i >= T
             U act = (tbits ^ (tbits >> 1)) & ((((U)1) << (L - 1 - T)) - (U)1);   // bonds T..L-2
+            if (SPLIT) act &= (((U)1) << (kp.split_ahi - T)) - (U)1;             // ... below split_ahi
             // full rounds of NB partner tiles without predication (the active set is uniform per
             // tile), then at most one predicated round for the remainder
             while (((L <= 31) ? __popc((unsigned)act) : __popcll((unsigned long long)act)) >= NB) {
@@ -216,7 +220,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
 template <int L>
 static cudaError_t launch_tiled(const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s) {
     constexpr int T = kTileBits;
-    if (a.work && heis_stream(L, a.M, a.bicg)) return launch_stream<L>(a, kp, J, grid, s);
+    if (a.work && heis_stream(L, a.M, a.bicg, kp.split_ahi > 0 && a.st)) return launch_stream<L>(a, kp, J, grid, s);
     const size_t shm = sizeof(cplx) << T;
     const bool p = a.st != nullptr;
     if (a.bicg) {
@@ -236,6 +240,8 @@ static cudaError_t launch_tiled(const SpmvArgs &a, const KParams &kp, double J, 
     }
     if (kp.world > 1)
         return launch_k(heisenberg_tiled_kernel<L, T, 1, true>, grid, kThreads, shm, s, p, a, kp, J);
+    if (kp.split_ahi > 0 && a.st)   // solver mode with the bond split: H_A only
+        return launch_k(heisenberg_tiled_kernel<L, T, 1, false, true>, grid, kThreads, shm, s, p, a, kp, J);
     return launch_k(heisenberg_tiled_kernel<L, T, 1, false>, grid, kThreads, shm, s, p, a, kp, J);
 }
 

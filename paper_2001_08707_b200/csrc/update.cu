@@ -447,6 +447,7 @@ static cudaError_t launch_update_nl(const KParams &kp, const cplx *q, const cplx
 }
 
 cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cudaStream_t s) {
+    if (kp.split_ahi > 0) return launch_update_split(kp, q, s);
     if (kp.nl > 4 && !kp.full) {
         if (kp.bicg)
             return launch_k(update_proj_kernel<true>, kp.nblk_upd + kp.n_agents, kThreads, 0, s, true, kp, q, qt);

@@ -1,0 +1,276 @@
+// update_split.cu — the bond-split iteration of the Heisenberg chain at large L (one GPU, COCG,
+// N_left = 1).
+//
+// H = H_A + H_B (EQ heisenberg P:L831: H = J sum_i S_i.S_{i+1}; every bond's off-diagonal part
+// flips the two spins, amplitude J/2).  H_A holds the diagonal and the bonds (i, i+1) with
+// i < AHI = L - HB; H_B the bonds i = AHI..L-2 and the periodic bond (L-1, 0).  The SpMV applies
+// H_A in natural order (spmv_stream.cuh, SPLIT): its bonds stay inside a 2^10-state tile or
+// reach a partner tile that is still in L2.  H_B would need partners 2^AHI states away — from
+// DRAM on every use — so this kernel applies it instead, in its own row order: a B-tile is the
+// 2^TB states {2^PB-state contiguous piece} x {all 2^HB combinations of spins AHI..L-1}, staged
+// in shared memory, so every H_B partner of a B-tile row is in the same B-tile.
+//
+// Per B-tile (one CTA, double-buffered cp.async staging of r_n):
+//   q_n     = q_A + H_B r_n                                   (q_A: the SpMV's output)
+//   r_{n+1} = (1 + c - alpha z_s) r_n + alpha q_n - c r_{n-1}  (EQ-CG-RN-3REC P:L269, stored form)
+//   dots of the next iteration: rho_{n+1} = <r_{n+1}, r_{n+1}>, ||r_{n+1}||^2, a^dag r_{n+1}
+//   w_B     = <r_{n+1}, H_B r_{n+1}>  (r_{n+1} parked in shared memory; each anti-aligned pair
+//            counted once, doubled)
+// so the next iteration's w_{n+1} = <r_{n+1}, H r_{n+1}> (EQ-REC-ALPHA-N2 P:L276) is w_A (SpMV
+// partials) + w_B (these partials): both sit in the half of part_w the next update's seed step
+// reduces, in fixed order.  Bytes per row: SpMV 32 (r, q_A) + update 80 (r_n, q_A, r_{n-1}, b
+// read; r_{n+1} written) = the algorithmic 112 of SURVEY §8(d.3): the far bonds' partner reads
+// (the pair kernel's 3.5x DRAM excess at L = 30) are gone.
+#include "kernels.cuh"
+#include "steps.cuh"
+
+namespace sk {
+
+constexpr int kSplitHB = 8;      // spins AHI..L-1 in a B-tile
+constexpr int kSplitTB = 12;     // 2^12 states per B-tile (64 KB per buffer, two buffers)
+constexpr int kSplitNT = 1024;   // threads per CTA (one CTA per SM)
+
+static __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+static __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+static __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Global row of B-tile t, local index e: piece bits e[0, PB) -> spins 0..PB-1, high bits
+// e[PB, TB) -> spins AHI..L-1, tile index t -> spins PB..AHI-1.
+template <int HB, int TB>
+static __device__ __forceinline__ int64_t split_row(int64_t t, int e, int ahi) {
+    constexpr int PB = TB - HB;
+    return ((int64_t)(e >> PB) << ahi) | (t << PB) | (int64_t)(e & ((1 << PB) - 1));
+}
+
+// sum of the H_B partners of local row e (bond (AHI+j, AHI+j+1) <-> local bits PB+j, PB+j+1;
+// periodic (L-1, 0) <-> local bits TB-1, 0): every anti-aligned bond contributes r[e ^ flip]
+template <int HB, int TB>
+static __device__ __forceinline__ cplx hb_partners(const cplx *S, int e) {
+    constexpr int PB = TB - HB;
+    cplx h = mk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < HB - 1; ++j)
+        if (((e >> (PB + j)) ^ (e >> (PB + j + 1))) & 1) {
+            const cplx p = S[e ^ (3 << (PB + j))];
+            h.x += p.x;
+            h.y += p.y;
+        }
+    if (((e >> (TB - 1)) ^ e) & 1) {
+        const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
+        h.x += p.x;
+        h.y += p.y;
+    }
+    return h;
+}
+
+// Each anti-aligned pair of H_B once (from the row whose lower bond bit is 0): the pair's two
+// terms r_e r_p J/2 + r_p r_e J/2 of <r, H_B r> are added as one product (caller doubles).
+template <int HB, int TB>
+static __device__ __forceinline__ cplx hb_pairs(const cplx *S, int e, cplx re) {
+    constexpr int PB = TB - HB;
+    cplx h = mk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < HB - 1; ++j)
+        if (!((e >> (PB + j)) & 1) && ((e >> (PB + j + 1)) & 1)) {
+            const cplx p = S[e ^ (3 << (PB + j))];
+            h.x += p.x;
+            h.y += p.y;
+        }
+    if (!(e & 1) && ((e >> (TB - 1)) & 1)) {
+        const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
+        h.x += p.x;
+        h.y += p.y;
+    }
+    return cmul(re, h);
+}
+
+template <int HB, int TB, int NT>
+static __device__ __forceinline__ void stage_tile(cplx *S, const cplx *__restrict__ r, int64_t t, int ahi) {
+    constexpr int TS = 1 << TB;
+#pragma unroll
+    for (int k = 0; k < TS / NT; ++k) {
+        const int e = threadIdx.x + k * NT;
+        cp_async16(S + e, r + split_row<HB, TB>(t, e, ahi));
+    }
+}
+
+// Seed scalars, as in update.cu (deferred mode: every CTA reduces the w partials — here w_A
+// groups + w_B partials — in fixed order and evaluates the seed step itself).
+struct SplitSeed {
+    DevState S;
+    SeedOut o;
+    int64_t nsx;
+    cplx red8[8];
+};
+
+template <int HB, int TB, int NT>
+__global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const cplx *__restrict__ q) {
+    constexpr int TS = 1 << TB, PER = TS / NT;
+    static_assert(PER * NT == TS && NT >= 256, "B-tile must be a multiple of the CTA");
+    extern __shared__ __align__(16) cplx S2[];   // [2][TS] staged r_n, then r_{n+1}
+    __shared__ ShiftScratch ss;
+    __shared__ SplitSeed us;
+    __shared__ cplx scratch[4 * (NT / 32)];
+    pdl_wait();
+    DevState *st = kp.st;
+    if (st->status != ST_ITERATING) return;
+    const int wb = blockIdx.x - kp.n_agents, nwb = gridDim.x - kp.n_agents;
+    const int ahi = kp.split_ahi;
+    const int64_t ntiles = kp.M >> TB;
+    const int64_t ns = st->n_started + 1;   // after the seed step of iteration n (deferred mode)
+    const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);   // r_n
+    const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);   // r_{n-1}
+    cplx *__restrict__ rn_ = pick3(kp.r, ns);             // r_{n+1}
+    // the first tile's r_n does not depend on the seed scalars: in flight during the w reduction
+    if (wb >= 0 && wb < ntiles) stage_tile<HB, TB, NT>(S2, rc_, wb, ahi);
+    cp_async_commit();
+    // ---- seed step (a3): w = w_A + w_B partials of this iteration's half, fixed order
+    {
+        const int64_t m = st->n_started;
+        state_load_nosync(us.S, st);
+        const cplx w = reduce_w_fixed(kp.part_w + (m & 1) * kp.wred_stride + kp.wred_off, kp.wred_n, us.red8);
+        if (threadIdx.x == 0) {
+            us.o = seed_compute(us.S, w);
+            us.nsx = m + 1;
+            if (blockIdx.x == 0) {
+                st->rec = us.o;
+                st->pending = 1;
+                if (us.o.ok) st->seq = m + 1;
+            }
+        }
+        __syncthreads();
+        if (!us.o.ok) {
+            cp_async_wait<0>();
+            return;
+        }
+    }
+    if (blockIdx.x < kp.n_agents) {   // shift agents (a4 + a6 + pending a8)
+        shift_step(kp, ss, blockIdx.x, us.o.alpha, us.o.beta, us.o.c);
+        return;
+    }
+    const cplx a_cur = us.o.a_cur, a_q = us.o.a_q, a_prev = us.o.a_prev;
+    const double hJ = 0.5 * kp.J;
+    const cplx *__restrict__ left = kp.left;
+    cplx rho = mk(0.0, 0.0), nu = mk(0.0, 0.0), g = mk(0.0, 0.0), wbp = mk(0.0, 0.0);
+    int it = 0;
+    for (int64_t t = wb; t < ntiles; t += nwb, ++it) {
+        cplx *S = S2 + (it & 1) * TS;
+        if (t + nwb < ntiles) stage_tile<HB, TB, NT>(S2 + ((it + 1) & 1) * TS, rc_, t + nwb, ahi);
+        cp_async_commit();
+        cp_async_wait<1>();   // this tile's r_n has landed (the next one stays in flight)
+        __syncthreads();
+        cplx o[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = threadIdx.x + k * NT;
+            const int64_t s = split_row<HB, TB>(t, e, ahi);
+            const cplx qa = ldg_cs(q + s), rp = ldg_cs(rp_ + s), lv = ldg_cs(left + s);
+            const cplx h = hb_partners<HB, TB>(S, e);
+            const cplx qf = mk(fma(hJ, h.x, qa.x), fma(hJ, h.y, qa.y));   // (H r_n)_s
+            cplx rn = cmul(a_cur, S[e]);
+            rn = cfma(a_q, qf, rn);
+            rn = cfma(a_prev, rp, rn);
+            rn_[s] = rn;
+            rho = cfma(rn, rn, rho);
+            nu.x = fma(rn.x, rn.x, fma(rn.y, rn.y, nu.x));
+            g = cfma_conj(lv, rn, g);
+            o[k] = rn;
+        }
+        __syncthreads();   // every H_B read of r_n is done: park r_{n+1} in its place
+#pragma unroll
+        for (int k = 0; k < PER; ++k) S[threadIdx.x + k * NT] = o[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) wbp = cadd(wbp, hb_pairs<HB, TB>(S, threadIdx.x + k * NT, o[k]));
+        __syncthreads();   // this buffer is refilled two tiles later
+    }
+    // CTA partials: rho, ||r||^2, a^dag r (part_u) and w_B (the next half of part_w)
+    wbp = mk(2.0 * hJ * wbp.x, 2.0 * hJ * wbp.y);
+    cplx v[4] = {rho, nu, g, wbp};
+    block_sum<4>(v, scratch);
+    if (threadIdx.x == 0) {
+        cplx *pu = kp.part_u + (int64_t)wb * 3;
+        pu[0] = v[0];
+        pu[1] = v[1];
+        pu[2] = v[2];
+        kp.part_w[(us.nsx & 1) * kp.wred_stride + kp.wsplit_off + wb] = v[3];
+    }
+}
+
+// w_B partials of r_0 = b (initialisation; half 0 of part_w, which the first update reduces):
+// the same B-tiles and per-CTA tile order as the update kernel.
+template <int HB, int TB, int NT>
+__global__ void __launch_bounds__(NT, 1) split_wb_kernel(KParams kp, const cplx *__restrict__ r, cplx *out) {
+    constexpr int TS = 1 << TB, PER = TS / NT;
+    extern __shared__ __align__(16) cplx S2[];
+    __shared__ cplx scratch[NT / 32];
+    const int ahi = kp.split_ahi;
+    const int64_t ntiles = kp.M >> TB;
+    cplx wbp = mk(0.0, 0.0);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        stage_tile<HB, TB, NT>(S2, r, t, ahi);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int e = threadIdx.x + k * NT;
+            wbp = cadd(wbp, hb_pairs<HB, TB>(S2, e, S2[e]));
+        }
+        __syncthreads();
+    }
+    const double hJ = 0.5 * kp.J;
+    cplx v[1] = {mk(2.0 * hJ * wbp.x, 2.0 * hJ * wbp.y)};
+    block_sum<1>(v, scratch);
+    if (threadIdx.x == 0) out[blockIdx.x] = v[0];
+}
+
+// ---- host side --------------------------------------------------------------------------------
+int split_ahi_for(int L, int64_t M, int world, int bicg, int full, int nl, int kind_heisenberg) {
+    static int en = -2;
+    if (en == -2) {
+        const char *e = getenv("SHIFTK_HEIS_SPLIT");
+        en = !e ? -1 : (e[0] == '0' ? 0 : 1);
+    }
+    if (en == 0 || !kind_heisenberg || world != 1 || bicg || full || nl != 1) return 0;
+    const int ahi = L - kSplitHB;
+    if (ahi < kTileBits || ahi < kSplitTB - kSplitHB || M != (int64_t(1) << L) || L > 31) return 0;
+    return (en == 1 || L >= 24) ? ahi : 0;
+}
+
+int split_blocks() { return sm_count(); }   // one CTA per SM (128 KB of staging each)
+
+static size_t split_smem() { return 2 * (sizeof(cplx) << kSplitTB); }
+
+static cudaError_t split_setup() {
+    static PerDevice once;
+    return once_per_device(once, [] {
+        cudaError_t e = cudaFuncSetAttribute(update_split_kernel<kSplitHB, kSplitTB, kSplitNT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem());
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(split_wb_kernel<kSplitHB, kSplitTB, kSplitNT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem());
+        return e;
+    });
+}
+
+cudaError_t launch_update_split(const KParams &kp, const cplx *q, cudaStream_t s) {
+    const cudaError_t e = split_setup();
+    if (e != cudaSuccess) return e;
+    return launch_k(update_split_kernel<kSplitHB, kSplitTB, kSplitNT>, kp.nblk_upd + kp.n_agents, kSplitNT,
+                    split_smem(), s, true, kp, q);
+}
+
+cudaError_t launch_split_init(const KParams &kp, cudaStream_t s) {
+    const cudaError_t e = split_setup();
+    if (e != cudaSuccess) return e;
+    split_wb_kernel<kSplitHB, kSplitTB, kSplitNT><<<kp.nblk_upd, kSplitNT, split_smem(), s>>>(
+        kp, kp.r[0], kp.part_w + kp.wsplit_off);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

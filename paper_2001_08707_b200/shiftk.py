@@ -32,7 +32,7 @@ EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_ru
            "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
            "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
            "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc", "sk_checkpoint",
-           "sk_restore", "sk_combine", "sk_gram"]
+           "sk_restore", "sk_combine", "sk_gram", "sk_get_info"]
 
 
 class ShiftkError(RuntimeError):
@@ -71,6 +71,12 @@ class sk_coeffs(ctypes.Structure):
                 ("n_active", ctypes.c_int64), ("status", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("z_seed", sk_cplx), ("alpha", sk_cplx), ("rho", sk_cplx), ("beta", sk_cplx),
                 ("seed_residual", ctypes.c_double)]
+
+
+class sk_info(ctypes.Structure):
+    _fields_ = [("split_ahi", ctypes.c_int32), ("spmv_ctas", ctypes.c_int32),
+                ("update_ctas", ctypes.c_int32), ("shift_agents", ctypes.c_int32),
+                ("arena_bytes", ctypes.c_int64)]
 
 
 class sk_profile(ctypes.Structure):
@@ -122,6 +128,7 @@ def load(path: str = LIB_PATH):
         "sk_checkpoint": [VP, VP, P(ctypes.c_size_t)],
         "sk_restore": [VP, VP, ctypes.c_size_t],
         "sk_get_profile": [VP, P(sk_profile), I32],
+        "sk_get_info": [VP, P(sk_info)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -386,6 +393,13 @@ class Solver:
                     spmv_count=c.spmv_count, n_active=c.n_active, status=c.status,
                     z_seed=cz(c.z_seed), alpha=cz(c.alpha), rho=cz(c.rho), beta=cz(c.beta),
                     seed_residual=c.seed_residual)
+
+    def info(self) -> dict:
+        """The execution plan sk_init chose (sk_get_info): bond split, CTA counts, arena size."""
+        i = sk_info()
+        _check(load().sk_get_info(self._h, ctypes.byref(i)), "sk_get_info")
+        return dict(split_ahi=i.split_ahi, spmv_ctas=i.spmv_ctas, update_ctas=i.update_ctas,
+                    shift_agents=i.shift_agents, arena_bytes=i.arena_bytes)
 
     def debug_timestamps(self) -> np.ndarray:
         out = np.zeros(16, dtype=np.int64)

@@ -291,16 +291,106 @@ def test_grouped_partials_window_and_determinism():
     assert g.coefficients() == h.coefficients()
 
 
-def test_tile_pairs_window_and_determinism():
-    """L=24: the streaming SpMV works on tile pairs across the top spin bit (each the other's
-    periodic partner); oracle window and bit-identical reruns."""
+def _subprocess(code: str, env_extra: dict, timeout: int = 900):
+    """Run `code` in a fresh interpreter (the SHIFTK_* switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root + os.pathsep + os.path.join(root, "tests"), **env_extra)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=timeout)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), (out.stdout[-2000:], out.stderr[-3000:])
+
+
+def test_bond_split_default_at_l24_window_and_determinism():
+    """L=24 with one left vector (a = b): the bond split is on by default — the
+    streaming SpMV applies the diagonal and bonds i < 16, the update the bonds 16..22 and the
+    periodic bond from its B-tiles.  Oracle window, bit-identical reruns."""
     p = synth.make_problem("c2", L=24, nz=8)
-    g, o, _, _ = run_window(p, 3)
+    g, o, _, _ = run_window(p, 4)
+    assert g.info()["split_ahi"] == 24 - 8
     h = make_solver(to_device(p))
-    for _ in range(3):
+    for _ in range(4):
         h.update()
     assert np.array_equal(g.residuals(), h.residuals())
     assert g.coefficients() == h.coefficients()
+
+
+SPLIT_FORCED = """
+import numpy as np, oracle, synth
+from paper_2001_08707_b200 import shiftk
+from paper_2001_08707_b200.device import make_solver, to_device
+from test_gpu_parity import run_window, proj_err, REL
+for L in (20, 21, 22):
+    p = synth.make_problem("c2", L=L, nz=64)
+    g, o, wr, wy = run_window(p, 40)
+    assert g.info()["split_ahi"] == L - 8, g.info()
+    # graph-captured sk_run == stepwise, bit for bit (fixed-order w_A + w_B partials)
+    n = g.iterations
+    h = make_solver(to_device(p))
+    h.run(n, poll_every=n)
+    assert np.array_equal(g.residuals(), h.residuals()) and np.array_equal(g.projections(), h.projections())
+    assert g.coefficients() == h.coefficients()
+# restart in split mode (the w_B partials of r_n travel in the checkpoint) against the oracle
+p = synth.make_problem("c2", L=20, nz=64)
+dp = to_device(p)
+a = make_solver(dp)
+a.run(10)
+blob = a.checkpoint()
+a.finalize()
+g = make_solver(dp)
+g.restore(blob)
+o = oracle.Oracle(p.method, p.b, p.z, left=p.left, tol=p.tol, itermax=p.itermax)
+for _ in range(10):
+    o.step(p.op)
+for n in range(10, 25):
+    assert g.update() == o.step(p.op)
+    rg, ro = g.residuals(), o.residuals()
+    assert np.all(np.abs(rg - ro) <= REL * ro), (n, np.max(np.abs(rg - ro) / ro))
+    assert np.all(proj_err(g.projections(), o.projections()) <= REL), n
+# converged run (C2's geometry scaled to L = 20 would take ~3000 iterations: L = 20, 16 shifts
+# far from the real axis converge fast) against the oracle
+import dataclasses
+q = dataclasses.replace(synth.make_problem("c2", L=20, nz=16), z=synth.make_problem("c2", L=20, nz=16).z + 0.5j)
+g = make_solver(to_device(q))
+assert g.run(q.itermax) == shiftk.CONVERGED
+o = oracle.Oracle(q.method, q.b, q.z, left=q.left, tol=q.tol, itermax=q.itermax)
+assert o.run(q.op, q.itermax) == oracle.CONVERGED
+assert np.all(proj_err(g.projections(), o.projections()) <= REL)
+assert np.all(g.residuals() < q.tol) and np.all(o.residuals() < q.tol)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("a_kernel", ["stream", "tiled"])
+def test_bond_split_forced_at_small_l(a_kernel):
+    """The bond split forced at L = 20, 21, 22 (SHIFTK_HEIS_SPLIT=1; H_A by the streaming SpMV
+    (SHIFTK_HEIS_STREAM=1, per-tile w partials) or the tiled one (per-CTA partials); AHI =
+    12..14, so the B-tiles cover 7 chain bonds + the periodic one and 2^8..2^10 B-tiles over 148
+    CTAs): 40-iteration oracle windows on 64 shifts, graph == stepwise bitwise, restart from a
+    checkpoint against the oracle, and a converged run."""
+    _subprocess(SPLIT_FORCED, {"SHIFTK_HEIS_SPLIT": "1", "SHIFTK_HEIS_STREAM": "1" if a_kernel == "stream" else "0"})
+
+
+def test_tile_pairs_window_and_determinism():
+    """L=24 with the bond split off (SHIFTK_HEIS_SPLIT=0): the streaming SpMV works on tile pairs
+    across the top spin bit (each the other's periodic partner); oracle window and bit-identical
+    reruns."""
+    _subprocess("""
+import numpy as np, synth
+from paper_2001_08707_b200.device import make_solver, to_device
+from test_gpu_parity import run_window
+p = synth.make_problem("c2", L=24, nz=8)
+g, o, _, _ = run_window(p, 3)
+assert g.info()["split_ahi"] == 0
+h = make_solver(to_device(p))
+for _ in range(3):
+    h.update()
+assert np.array_equal(g.residuals(), h.residuals())
+assert g.coefficients() == h.coefficients()
+print("ok")
+""", {"SHIFTK_HEIS_SPLIT": "0"})
 
 
 def test_many_shifts_beyond_the_shared_memory_flags():

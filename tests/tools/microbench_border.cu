@@ -119,14 +119,16 @@ __device__ __forceinline__ void cpa16(void *dst, const void *src) {
 template <int L, int AHI, int PB, int NT>
 __global__ void __launch_bounds__(NT, 1) bord2(const cplx *__restrict__ rc, const cplx *__restrict__ rp,
                                                const cplx *__restrict__ q, const cplx *__restrict__ b,
-                                               cplx *__restrict__ rn, double2 *part) {
+                                               cplx *__restrict__ rn, double2 *part, int64_t pad) {
     constexpr int HB = L - AHI, TB = PB + HB, TS = 1 << TB, PER = TS / NT;
     static_assert(PER * NT == TS, "");
     extern __shared__ cplx S2[];   // [2][TS]
     const int64_t ntiles = int64_t(1) << (AHI - PB);
     const int tid = threadIdx.x;
     double wx = 0, wy = 0, ax = 0;
-    auto row = [&](int64_t t, int e) { return ((int64_t)(e >> PB) << AHI) | (t << PB) | (e & ((1 << PB) - 1)); };
+    // high-bit segments of 2^AHI rows stored `pad` rows apart (pad 0: the natural layout)
+    const int64_t seg = (int64_t(1) << AHI) + pad;
+    auto row = [&](int64_t t, int e) { return (int64_t)(e >> PB) * seg + (t << PB) + (e & ((1 << PB) - 1)); };
     int64_t t = blockIdx.x;
     if (t < ntiles)
         for (int k = 0; k < PER; ++k) cpa16(S2 + tid + k * NT, rc + row(t, tid + k * NT));
@@ -191,6 +193,24 @@ __global__ void __launch_bounds__(NT, 1) bord2(const cplx *__restrict__ rc, cons
     if (wx + ax == 1234.5) part[0] = make_double2(wx, wy);
 }
 
+// Pure B-order streaming (no shared memory, no bonds): the DRAM-pattern cost of the piece size.
+template <int L, int AHI, int PB>
+__global__ void bpure(const cplx *__restrict__ rc, const cplx *__restrict__ rp, const cplx *__restrict__ q,
+                      const cplx *__restrict__ b, cplx *__restrict__ rn, int64_t M, double2 *part) {
+    constexpr int HB = L - AHI, TB = PB + HB;
+    double ax = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(i & ((1 << TB) - 1));
+        const int64_t t = i >> TB;
+        const int64_t s = ((int64_t)(e >> PB) << AHI) | (t << PB) | (e & ((1 << PB) - 1));
+        cplx a = ldcs(rc + s), c = ldcs(rp + s), d = ldcs(q + s), f = ldcs(b + s);
+        cplx o = make_double2(0.5 * a.x + 0.25 * d.x - 0.125 * c.x, 0.5 * a.y + 0.25 * d.y - 0.125 * c.y);
+        __stcs(rn + s, o);
+        ax += o.x * f.x + o.y * f.y;
+    }
+    if (ax == 1234.5) part[0] = make_double2(ax, ax);
+}
+
 static float timeit(void (*f)(void *), void *arg, int reps) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -211,6 +231,7 @@ struct Bufs {
     unsigned long long *work;
     int64_t M;
     int grid, dyn;
+    int64_t pad;
 };
 static Bufs G;
 
@@ -239,43 +260,51 @@ static void bench(int ctas) {
 template <int L, int AHI, int PB, int NT>
 static void run_b2(void *) {
     constexpr int TS = 1 << (PB + L - AHI);
-    bord2<L, AHI, PB, NT><<<G.grid, NT, 2 * TS * sizeof(cplx)>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.part);
+    bord2<L, AHI, PB, NT><<<G.grid, NT, 2 * TS * sizeof(cplx)>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.part, G.pad);
 }
 template <int L, int AHI, int PB, int NT>
-static void bench2(int ctas) {
+static void bench2(int ctas, int64_t pad = 0) {
+    G.pad = pad;
     constexpr int TS = 1 << (PB + L - AHI);
     cudaFuncSetAttribute(bord2<L, AHI, PB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TS * (int)sizeof(cplx));
     G.grid = 148 * ctas;
     float ms = timeit(run_b2<L, AHI, PB, NT>, nullptr, 3);
     cudaError_t e = cudaGetLastError();
-    printf("B-order/cp.async x2 L=%d AHI=%d PB=%d (piece %4d B, tile %3d KB) NT=%4d ctas/SM=%d: %8.3f ms  %7.1f GB/s  %s\n", L, AHI, PB,
-           16 << PB, TS * 16 / 1024, NT, ctas, ms, 80.0 * G.M / (ms * 1e6), cudaGetErrorString(e));
+    printf("B-order/cp.async x2 L=%d AHI=%d PB=%d (piece %4d B, tile %3d KB) NT=%4d ctas/SM=%d pad=%7lld rows: %8.3f ms  %7.1f GB/s  %s\n", L, AHI, PB,
+           16 << PB, TS * 16 / 1024, NT, ctas, (long long)pad, ms, 80.0 * G.M / (ms * 1e6), cudaGetErrorString(e));
+}
+
+template <int L, int AHI, int PB>
+static void run_p(void *) { bpure<L, AHI, PB><<<148 * 8, 256>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.M, G.part); }
+template <int L, int AHI, int PB>
+static void benchp() {
+    float ms = timeit(run_p<L, AHI, PB>, nullptr, 3);
+    printf("pure B-order L=%d AHI=%d PB=%d (piece %4d B, tile %d states): %8.3f ms  %7.1f GB/s  %s\n", L, AHI, PB, 16 << PB,
+           1 << (PB + L - AHI), ms, 80.0 * G.M / (ms * 1e6), cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
     G.M = int64_t(1) << 30;
+    const int64_t alloc = G.M + 512 * ((int64_t(1) << 17) + 4096);   // room for padded layouts
     for (int i = 0; i < 5; ++i) {
-        if (cudaMalloc(&G.v[i], G.M * sizeof(cplx)) != cudaSuccess) { printf("alloc failed\n"); return 1; }
-        cudaMemset(G.v[i], 0, G.M * sizeof(cplx));
+        if (cudaMalloc(&G.v[i], alloc * sizeof(cplx)) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+        cudaMemset(G.v[i], 0, alloc * sizeof(cplx));
     }
     cudaMalloc(&G.part, 64);
     cudaMalloc(&G.work, 64);
     float ms = timeit(run_lin, nullptr, 3);
     printf("linear update                      : %8.3f ms  %7.1f GB/s\n", ms, 80.0 * G.M / (ms * 1e6));
-    bench<30, 21, 4, 1024>(1);
-    bench<30, 21, 4, 512>(1);
-    bench<30, 21, 3, 512>(2);
-    bench<30, 21, 3, 256>(3);
-    bench<30, 22, 4, 512>(2);
-    bench<30, 21, 5, 1024>(1);   // 256 KB: does not fit (expect an error)
-    bench<30, 20, 3, 1024>(1);
-    bench<30, 19, 2, 1024>(1);
-    bench2<30, 21, 3, 512>(1);
-    bench2<30, 21, 3, 1024>(1);
-    bench2<30, 22, 4, 512>(1);
+    benchp<30, 21, 2>();
+    benchp<30, 21, 3>();
+    benchp<30, 21, 4>();
+    benchp<30, 21, 5>();
+    benchp<30, 21, 6>();
+    benchp<30, 22, 3>();
+    benchp<30, 22, 4>();
+    benchp<30, 22, 5>();
+    benchp<30, 24, 4>();
+    benchp<30, 26, 4>();
     bench2<30, 22, 4, 1024>(1);
-    bench2<30, 21, 2, 512>(2);
-    bench2<30, 22, 3, 512>(2);
-    bench2<30, 23, 4, 512>(2);
+    bench2<30, 23, 5, 1024>(1);
     return 0;
 }
