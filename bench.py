@@ -4,19 +4,26 @@
 A step is one full iteration of shifted COCG/BiCG (seed SpMV with
 fused dot, scalar recurrences + retirement + seed switch, fused three-term update with the
 next-iteration dots and the per-shift projected / full update) over the config's synthetic
-input.  Default workload: C2 (BASELINE.json configs[1]) — Heisenberg L=20, M=2^20, N_z=1024,
-a=b projection, COCG, complex128.
+input.  Default workload: C5 (BASELINE.json configs[4], the largest single-GPU config and the
+north star's HBM / scaling config) — Heisenberg L=30, M=2^30, N_z=512, a=b projection, COCG,
+complex128; `--config c1..c5` selects another (C2 is the latency-bound configs[1]).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-Timing: W untimed iterations, then K iterations each bracketed by CUDA events on the solver's
-stream, with L2 flushed (256 MiB write) before every step outside the events; barrier +
-synchronize around the timed region; max over ranks.  Clocks are sampled with NVML every 2 ms
-(nvidia-smi where NVML is missing) during the timed region.  `value` comes from a pass with nothing between the kernels; a second
-pass of the same K flushed steps records CUDA events around every kernel (on the solver's
-stream) for the per-kernel durations behind `roofline` (events between the kernels cost the
-programmatic-launch overlap, ~10 us per step at C2, so that pass is not the value).  `--impl reference` times the CPU oracle (oracle/) on the same
-workload (the reference arm of this tier: the paper has no code).
+Timing: W untimed iterations, then three passes of K iterations, each step
+bracketed by CUDA events on the solver's stream with L2 flushed (256 MiB write) before every
+step outside the events; barrier + synchronize around each pass; max over ranks; `value` is the
+median pass.  Clocks are sampled with NVML every 2 ms (nvidia-smi where NVML is missing) during
+the timed passes.  A fourth pass of the same K flushed steps records CUDA events around every
+kernel (on the solver's stream) for the per-kernel durations behind `roofline` (events between
+the kernels cost the programmatic-launch overlap, so that pass is not the value).
+
+CPU legs (the oracle, oracle/, test infrastructure timed as it stands): `cpu_baseline` runs the
+OpenMP build on all host cores over the first iterations of the full-size workload (a bounded
+sample, ~20 s); `cpu_baseline_1core` runs the one-thread build on a scaled instance of the same
+config (16x fewer rows, same shifts) and extrapolates to the full size (the oracle's cost is
+linear in M; labelled as such).  `--impl reference` times the OpenMP oracle on the workload itself
+(the reference arm of this tier: the paper has no code).
 """
 from __future__ import annotations
 
@@ -182,11 +189,11 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------ oracle legs
 
-def oracle_sample(problem, budget_s: float, max_iters: int):
-    """Time the CPU oracle (as it stands) on the first iterations of the workload."""
+def oracle_sample(problem, budget_s: float, max_iters: int, omp: bool):
+    """Time the CPU oracle (as it stands) on the first iterations of `problem` (at least one)."""
     import oracle
     o = oracle.Oracle(problem.method, problem.b, problem.z, left=problem.left,
-                      full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax)
+                      full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax, omp=omp)
     t0 = time.perf_counter()
     its = 0
     while its < max_iters:
@@ -195,7 +202,43 @@ def oracle_sample(problem, budget_s: float, max_iters: int):
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
+    o.close()
     return its, dt
+
+
+def scaled_sample(name: str, problem):
+    """A 16x smaller instance of the same config (same shifts, same generator recipe), for the
+    one-thread oracle leg; None when the config has no size knob."""
+    if name in ("c1", "c2", "c5"):
+        return synth.make_problem(name, L=problem.op["L"] - 4)
+    if name == "c3":
+        return synth.make_problem(name, M=problem.M >> 4)
+    if name == "c4":
+        return synth.make_problem(name, W=int(round(math.sqrt(problem.M))) >> 2)
+    return None
+
+
+def cpu_legs(args, problem):
+    """cpu_baseline (OpenMP, all cores, full size) and cpu_baseline_1core (scaled, extrapolated)."""
+    import oracle
+    out = {}
+    its, dt = oracle_sample(problem, args.cpu_budget, 400, omp=True)
+    out["cpu_baseline"] = {
+        "value": problem.n_shift * its / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+        "host": host_info(), "build": "OpenMP (static chunks, chunk partials combined in index order)",
+        "sample": f"first {its} iterations of {problem.name} at full size (M={problem.M}), {dt:.1f} s "
+                  f"on {oracle.threads()} threads"}
+    base = problem.name.split("[")[0]
+    small = scaled_sample(base, problem) if problem.M >= (1 << 22) else problem
+    if small is not None:
+        its1, dt1 = oracle_sample(small, args.cpu_budget, 400, omp=False)
+        v = small.n_shift * its1 / dt1 * (small.M / problem.M)
+        out["cpu_baseline_1core"] = {
+            "value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_info(),
+            "sample": (f"first {its1} iterations of {small.name} (M={small.M}), {dt1:.1f} s on one thread"
+                       + ("" if small is problem else
+                          f"; extrapolated to M={problem.M} by M_sample/M (oracle cost is linear in M)"))}
+    return out
 
 
 def run_reference(args, problem):
@@ -204,22 +247,24 @@ def run_reference(args, problem):
         return
     import oracle
     o = oracle.Oracle(problem.method, problem.b, problem.z, left=problem.left,
-                      full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax)
+                      full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax, omp=True)
     for _ in range(args.warmup):
         o.step(problem.op)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         o.step(problem.op)
     dt = time.perf_counter() - t0
+    o.close()
     val = problem.n_shift * args.steps / dt
     sample = (f"{problem.name}: oracle iterations {args.warmup}..{args.warmup + args.steps - 1} "
-              f"of the full-size workload (M={problem.M}, N_z={problem.n_shift})")
+              f"of the full-size workload (M={problem.M}, N_z={problem.n_shift}), OpenMP on "
+              f"{oracle.threads()} threads")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "config": config_dict(problem, 1),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-                             "host": host_info()},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -235,7 +280,13 @@ def host_info():
                     break
     except OSError:
         pass
-    return {"cpu": model, "nproc": os.cpu_count()}
+    mem = None
+    try:
+        with open("/proc/meminfo") as f:
+            mem = round(int(f.readline().split()[1]) / 2 ** 20, 1)
+    except (OSError, ValueError, IndexError):
+        pass
+    return {"cpu": model, "nproc": os.cpu_count(), "ram_gib": mem}
 
 
 def config_dict(problem, world):
@@ -254,11 +305,12 @@ def config_dict(problem, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle time")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle time per CPU leg")
+    ap.add_argument("--repeats", type=int, default=3, help="timed passes (value = the median)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -313,18 +365,25 @@ def main():
             dist.barrier()
         return float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
 
-    # pass 1 (the value): no instrumentation between the kernels
+    # passes 1..R (the value = the median pass): no instrumentation between the kernels
     n0 = solver.coefficients()["iterations"]   # (may launch the pending finish: before the count)
     launches0 = solver.profile()["launches"]
+    passes = []
     with ClockSampler(local) as clk:
-        total_ms = timed_pass()
-    launches = solver.profile()["launches"] - launches0
-    # active shift-iterations of the timed window: shift k is updated in
-    # iteration m while m < retired_at[k]
+        for _ in range(max(1, args.repeats)):
+            passes.append(timed_pass())
+    launches = (solver.profile()["launches"] - launches0) // max(1, args.repeats)
+    if world > 1:
+        t = torch.tensor(passes, device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        passes = [float(v) for v in t.tolist()]
+    total_ms = statistics.median(passes)
+    # active shift-iterations of the timed windows: shift k is updated in
+    # iteration m while m < retired_at[k] (per pass: the mean over the passes)
     n1 = solver.coefficients()["iterations"]
     _, _, ret = solver.shift_state()
     stop = np.where(ret >= 0, np.minimum(ret, n1), n1)
-    active_its = int(np.clip(stop - n0, 0, None).sum())
+    active_its = int(np.clip(stop - n0, 0, None).sum()) / max(1, args.repeats)
     # pass 2 (the kernel shares): the same K steps with CUDA events around each kernel on the
     # solver's stream (the events cost the programmatic launch overlap, so not the value)
     solver.profile_enable(True)
@@ -333,10 +392,6 @@ def main():
     prof = solver.profile(reset=True)
     solver.profile_enable(False)
     coeffs = solver.coefficients()
-    if world > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
     value = problem.n_shift * args.steps / (total_ms * 1e-3)   # one global problem (strong scaling)
 
     # roofline of the dominant kernel (per launch: algorithmic bytes / mean device duration)
@@ -369,10 +424,19 @@ def main():
         "iteration_gbs_model_frac": iter_bytes / (total_ms / args.steps * 1e-3) / 1e9 / peak,
         "active_shift_iterations_per_s": active_its / (total_ms * 1e-3),
         "gpu_launches": launches,
+        "passes_ms": passes,
+        "plan": solver.info(),
         "solver_state": {"iterations": coeffs["iterations"], "n_active": coeffs["n_active"],
                          "switches": coeffs["switches"]},
     }
     line["clocks"] = clk.summary()
+    if world > 1:   # exchange volume of the SpMV: other ranks' rows read over NVLink (dist.py model)
+        from paper_2001_08707_b200 import dist as skdist_model
+        per = [skdist_model.remote_rows_per_spmv(problem, world, g) * 16 * (2 if problem.method == "bicg" else 1)
+               for g in range(world)]
+        line["nvlink_bytes_per_rank"] = {"max": max(per), "per_rank": per,
+                                         "model": "element reads of other ranks' rows per iteration "
+                                                  "(paper_2001_08707_b200/dist.py remote_rows_per_spmv)"}
 
     # end-to-end through the public API with HOST buffers (pinned b in, results out)
     if not args.no_e2e:
@@ -405,12 +469,7 @@ def main():
                        "note": "sk_init(host b) + sk_run(K) + sk_get_projection/residual + finalize"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        its, dt = oracle_sample(problem, args.cpu_budget, 400)
-        line["cpu_baseline"] = {"value": problem.n_shift * its / dt, "unit": UNIT, "cores": 1,
-                                "host": host_info(),
-                                "kind": "oracle",
-                                "sample": f"first {its} iterations of {problem.name} (full size), "
-                                          f"{dt:.1f} s single-threaded"}
+        line.update(cpu_legs(args, problem))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -17,6 +17,7 @@
 // Multi-rank (MULTI): the partner tile's address comes from the shard table — a bulk copy
 // straight from the owning rank's buffer (peer memory), fused into the same pipeline.
 #pragma once
+#include "async_copy.cuh"
 #include "spmv_common.cuh"
 
 namespace sk {
@@ -24,29 +25,6 @@ namespace sk {
 constexpr int kStreamConsumers = 256;            // 8 consumer warps
 constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
 constexpr int kStreamSlots = 4;                  // partner ring depth (tiles)
-
-static __device__ __forceinline__ uint32_t sa(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-static __device__ __forceinline__ void mb_init(uint64_t *b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count) : "memory");
-}
-static __device__ __forceinline__ void mb_expect(uint64_t *b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
-}
-static __device__ __forceinline__ void mb_arrive(uint64_t *b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
-}
-static __device__ __forceinline__ void mb_wait(uint64_t *b, unsigned parity) {
-    unsigned done = 0;
-    while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(sa(b)), "r"(parity) : "memory");
-}
-static __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(b)) : "memory");
-}
 
 // active tile-level bonds T..L-2 of the tile with global first state `base` (bit j = bond j+T)
 template <int L, int T, typename U>

@@ -28,7 +28,7 @@ namespace sk {
 
 constexpr int kSplitHB = 8;      // spins AHI..L-1 in a B-tile
 constexpr int kSplitTB = 12;     // 2^12 states per B-tile (64 KB per buffer, two buffers)
-constexpr int kSplitNT = 1024;   // threads per CTA (one CTA per SM)
+constexpr int kSplitNT = 512;    // threads per CTA (one CTA per SM)
 
 static __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -156,28 +156,43 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
     const double hJ = 0.5 * kp.J;
     const cplx *__restrict__ left = kp.left;
     cplx rho = mk(0.0, 0.0), nu = mk(0.0, 0.0), g = mk(0.0, 0.0), wbp = mk(0.0, 0.0);
+    // row of local index e = tid + k NT in B-tile t: row0 + k kstep + (t << PB) (NT is a multiple
+    // of the piece, so k moves whole pieces: (NT >> PB) high-bit steps of 2^AHI rows)
+    constexpr int PB = TB - HB;
+    static_assert(NT % (1 << PB) == 0, "a thread's rows sit at the same offset in their pieces");
+    const int64_t row0 = split_row<HB, TB>(0, threadIdx.x, ahi);
+    const int64_t kstep = (int64_t)(NT >> PB) << ahi;
     int it = 0;
     for (int64_t t = wb; t < ntiles; t += nwb, ++it) {
         cplx *S = S2 + (it & 1) * TS;
         if (t + nwb < ntiles) stage_tile<HB, TB, NT>(S2 + ((it + 1) & 1) * TS, rc_, t + nwb, ahi);
         cp_async_commit();
+        // every row-stream load of the tile is issued before waiting for its staged r_n (they do
+        // not depend on it): 3 PER loads in flight per thread across the wait and the barrier
+        const int64_t rt = row0 + (t << PB);
+        cplx qa[PER], rp[PER], lv[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int64_t s = rt + k * kstep;
+            qa[k] = ldg_cs(q + s);
+            rp[k] = ldg_cs(rp_ + s);
+            lv[k] = ldg_cs(left + s);
+        }
         cp_async_wait<1>();   // this tile's r_n has landed (the next one stays in flight)
         __syncthreads();
         cplx o[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int e = threadIdx.x + k * NT;
-            const int64_t s = split_row<HB, TB>(t, e, ahi);
-            const cplx qa = ldg_cs(q + s), rp = ldg_cs(rp_ + s), lv = ldg_cs(left + s);
             const cplx h = hb_partners<HB, TB>(S, e);
-            const cplx qf = mk(fma(hJ, h.x, qa.x), fma(hJ, h.y, qa.y));   // (H r_n)_s
+            const cplx qf = mk(fma(hJ, h.x, qa[k].x), fma(hJ, h.y, qa[k].y));   // (H r_n)_s
             cplx rn = cmul(a_cur, S[e]);
             rn = cfma(a_q, qf, rn);
-            rn = cfma(a_prev, rp, rn);
-            rn_[s] = rn;
+            rn = cfma(a_prev, rp[k], rn);
+            rn_[rt + k * kstep] = rn;
             rho = cfma(rn, rn, rho);
             nu.x = fma(rn.x, rn.x, fma(rn.y, rn.y, nu.x));
-            g = cfma_conj(lv, rn, g);
+            g = cfma_conj(lv[k], rn, g);
             o[k] = rn;
         }
         __syncthreads();   // every H_B read of r_n is done: park r_{n+1} in its place

@@ -88,3 +88,39 @@ def connect(solver, pg=None):
     from .shiftk import nccl_unique_id
     handles, nid = exchange_handles(solver.ipc_handle(), nccl_unique_id, pg)
     solver.connect(handles, nid)
+
+
+def remote_rows_per_spmv(problem, world: int, rank: int) -> int:
+    """Rows of OTHER ranks this rank's SpMV reads per application (each a 16-B complex128 read
+    over NVLink; element count, the algorithmic exchange volume of SURVEY §8(e)).
+
+    Heisenberg chain (rank = top log2(world) spin bits): a bond (i, i+1 mod L) reaches another
+    rank iff it flips a rank bit; for a bond between a rank bit and a local bit, half of the local
+    rows have it anti-aligned; for a bond between two rank bits, all rows or none (fixed by the
+    rank).  CSR: the stored entries of the local rows whose column lies outside them."""
+    row0, ml = shard_rows(problem.M, world, rank)
+    if world == 1:
+        return 0
+    op = problem.op
+    if op["kind"] == "heisenberg":
+        L = int(op["L"])
+        k = world.bit_length() - 1
+        top = set(range(L - k, L))
+        g = rank
+        n = 0
+        for i in range(L):
+            a, b = i, (i + 1) % L
+            if a not in top and b not in top:
+                continue
+            if a in top and b in top:
+                ga, gb = (g >> (a - (L - k))) & 1, (g >> (b - (L - k))) & 1
+                n += ml if ga != gb else 0
+            else:
+                n += ml // 2
+        return n
+    if op["kind"] in ("csr_real", "csr_cplx"):
+        rp = op["row_ptr"]
+        col = op["col"][int(rp[row0]):int(rp[row0 + ml])]
+        return int(np.count_nonzero((col < row0) | (col >= row0 + ml)))
+    raise ValueError(f"no exchange model for operator kind {op['kind']}")
+

@@ -101,3 +101,30 @@ def test_handshake_protocol(results):
     assert h0 == h1 == bytes([1]) * 64 + bytes([2]) * 64     # rank order
     assert id0 == id1 == bytes([7]) * 128                     # one id, shared
     assert calls0 == 1 and calls1 == 0                        # made on rank 0 only
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_remote_rows_model_matches_enumeration(world):
+    """The NVLink exchange model (dist.remote_rows_per_spmv, reported by bench.py for N > 1)
+    against a brute-force count of the off-rank partners of every local row (L = 10 chain; an
+    8-rank CSR with random columns)."""
+    import numpy as np
+    import synth
+    from paper_2001_08707_b200 import dist
+    p = synth.make_problem("c2", L=10, nz=2)
+    L, M = 10, 1 << 10
+    ml = M // world
+    for rank in range(world):
+        n = 0
+        for s in range(rank * ml, (rank + 1) * ml):
+            for i in range(L):
+                j = (i + 1) % L
+                if ((s >> i) ^ (s >> j)) & 1:
+                    n += ((s ^ (1 << i) ^ (1 << j)) // ml) != rank
+        assert dist.remote_rows_per_spmv(p, world, rank) == n
+    q = synth.make_problem("c3", M=1 << 12, nz=2)
+    for rank in range(world):
+        r0, r1 = rank * (q.M // world), (rank + 1) * (q.M // world)
+        rp, col = q.op["row_ptr"], q.op["col"]
+        n = sum(int(not (r0 <= c < r1)) for c in col[rp[r0]:rp[r1]])
+        assert dist.remote_rows_per_spmv(q, world, rank) == n

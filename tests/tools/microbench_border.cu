@@ -211,6 +211,104 @@ __global__ void bpure(const cplx *__restrict__ rc, const cplx *__restrict__ rp, 
     if (ax == 1234.5) part[0] = make_double2(ax, ax);
 }
 
+
+// ---- v3 variants (the update_split2 structure): staging by 16-B cp.async per row or by one
+// cp.async.bulk per piece (mbarrier), row streams by 128-bit or 256-bit (pair) loads
+__device__ __forceinline__ uint32_t sa3(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbi(uint64_t *b) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa3(b)) : "memory"); }
+__device__ __forceinline__ void mbx(uint64_t *b, unsigned n) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa3(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbw(uint64_t *b, unsigned ph) { unsigned d = 0; while (!d) asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }" : "=r"(d) : "r"(sa3(b)), "r"(ph) : "memory"); }
+__device__ __forceinline__ void bulk3(void *d, const void *s, unsigned n, uint64_t *b) { asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa3(d)), "l"(s), "r"(n), "r"(sa3(b)) : "memory"); }
+__device__ __forceinline__ void ld2(const cplx *p, cplx &a, cplx &b) { asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p)); }
+__device__ __forceinline__ void st2(cplx *p, cplx a, cplx b) { asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory"); }
+
+template <int L, int AHI, int PB, int NT, bool BULK, bool LD256, bool EARLY = false>
+__global__ void __launch_bounds__(NT, 1) bord3(const cplx *__restrict__ rc, const cplx *__restrict__ rp,
+                                               const cplx *__restrict__ q, const cplx *__restrict__ b,
+                                               cplx *__restrict__ rn, double2 *part) {
+    constexpr int HB = L - AHI, TB = PB + HB, TS = 1 << TB, NPIECE = 1 << HB;
+    constexpr int G = LD256 ? 2 : 1, PER = TS / G / NT;
+    extern __shared__ __align__(16) cplx S3[];
+    __shared__ uint64_t full[2];
+    const int64_t ntiles = int64_t(1) << (AHI - PB);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    auto row = [&](int64_t t, int e) { return ((int64_t)(e >> PB) << AHI) | (t << PB) | (e & ((1 << PB) - 1)); };
+    if (tid == 0) { mbi(&full[0]); mbi(&full[1]); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    __syncthreads();
+    auto stage = [&](int64_t t, int k) {
+        if (BULK) {
+            if (warp == 0) {
+                if (lane == 0) mbx(&full[k], TS * 16);
+                __syncwarp();
+                for (int h = lane; h < NPIECE; h += 32) bulk3(S3 + k * TS + (h << PB), rc + (t << PB) + ((int64_t)h << AHI), 16u << PB, &full[k]);
+            }
+        } else {
+            for (int j = 0; j < TS / NT; ++j) cpa16(S3 + k * TS + tid + j * NT, rc + row(t, tid + j * NT));
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    };
+    double wx = 0, ax = 0;
+    int64_t t = blockIdx.x;
+    if (t < ntiles) stage(t, 0);
+    for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
+        const int k = it & 1;
+        cplx *S = S3 + k * TS;
+        if (t + gridDim.x < ntiles) stage(t + gridDim.x, k ^ 1);
+        cplx QA[PER][G], C[PER][G], D[PER][G];
+        auto loads = [&]() {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int64_t s = row(t, (tid + j * NT) * G);
+                if (LD256) { ld2(q + s, QA[j][0], QA[j][1]); ld2(rp + s, C[j][0], C[j][1]); ld2(b + s, D[j][0], D[j][1]); }
+                else { QA[j][0] = ldcs(q + s); C[j][0] = ldcs(rp + s); D[j][0] = ldcs(b + s); }
+            }
+        };
+        if (EARLY) loads();
+        if (BULK) mbw(&full[k], (it >> 1) & 1);
+        else {
+            if (t + gridDim.x < ntiles) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+        }
+        if (!EARLY) loads();
+        cplx o[PER][G];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int e0 = (tid + j * NT) * G;
+            const int64_t s = row(t, e0);
+            cplx *qa = QA[j], *c = C[j], *d = D[j];
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                const int e = e0 + m;
+                cplx h = qa[m];
+#pragma unroll
+                for (int jj = 0; jj < HB - 1; ++jj)
+                    if (((e >> (PB + jj)) ^ (e >> (PB + jj + 1))) & 1) { const cplx p = S[e ^ (3 << (PB + jj))]; h.x += 0.5 * p.x; h.y += 0.5 * p.y; }
+                if (((e >> (TB - 1)) ^ e) & 1) { const cplx p = S[e ^ ((1 << (TB - 1)) | 1)]; h.x += 0.5 * p.x; h.y += 0.5 * p.y; }
+                const cplx v = S[e];
+                o[j][m] = make_double2(0.5 * v.x + 0.25 * h.x - 0.125 * c[m].x, 0.5 * v.y + 0.25 * h.y - 0.125 * c[m].y);
+                ax += o[j][m].x * d[m].x + o[j][m].y * d[m].y;
+            }
+            if (LD256) st2(rn + s, o[j][0], o[j][1]); else __stcs(rn + s, o[j][0]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) for (int m = 0; m < G; ++m) S[(tid + j * NT) * G + m] = o[j][m];
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) for (int m = 0; m < G; ++m) {
+            const int e = (tid + j * NT) * G + m;
+            cplx h = make_double2(0, 0);
+#pragma unroll
+            for (int jj = 0; jj < HB - 1; ++jj)
+                if (!((e >> (PB + jj)) & 1) && ((e >> (PB + jj + 1)) & 1)) { const cplx p = S[e ^ (3 << (PB + jj))]; h.x += p.x; h.y += p.y; }
+            wx += o[j][m].x * h.x - o[j][m].y * h.y;
+        }
+        __syncthreads();
+    }
+    if (wx + ax == 1234.5) part[0] = make_double2(wx, ax);
+}
+
 static float timeit(void (*f)(void *), void *arg, int reps) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -283,6 +381,18 @@ static void benchp() {
            1 << (PB + L - AHI), ms, 80.0 * G.M / (ms * 1e6), cudaGetErrorString(cudaGetLastError()));
 }
 
+template <bool BULK, bool LD256, int NT, bool EARLY>
+static void run_b3(void *) {
+    bord3<30, 22, 4, NT, BULK, LD256, EARLY><<<148, NT, 2 * 4096 * 16>>>(G.v[0], G.v[1], G.v[2], G.v[3], G.v[4], G.part);
+}
+template <bool BULK, bool LD256, int NT, bool EARLY = false>
+static void bench3() {
+    cudaFuncSetAttribute(bord3<30, 22, 4, NT, BULK, LD256, EARLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 16);
+    float ms = timeit(run_b3<BULK, LD256, NT, EARLY>, nullptr, 3);
+    printf("v3 AHI=22 PB=4 NT=%d staging=%s loads=%s early=%d: %8.3f ms  %7.1f GB/s  %s\n", NT, BULK ? "bulk/piece" : "cp.async16",
+           LD256 ? "256-bit" : "128-bit", (int)EARLY, ms, 80.0 * G.M / (ms * 1e6), cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
     G.M = int64_t(1) << 30;
     const int64_t alloc = G.M + 512 * ((int64_t(1) << 17) + 4096);   // room for padded layouts
@@ -294,17 +404,14 @@ int main() {
     cudaMalloc(&G.work, 64);
     float ms = timeit(run_lin, nullptr, 3);
     printf("linear update                      : %8.3f ms  %7.1f GB/s\n", ms, 80.0 * G.M / (ms * 1e6));
-    benchp<30, 21, 2>();
-    benchp<30, 21, 3>();
-    benchp<30, 21, 4>();
-    benchp<30, 21, 5>();
-    benchp<30, 21, 6>();
-    benchp<30, 22, 3>();
-    benchp<30, 22, 4>();
-    benchp<30, 22, 5>();
-    benchp<30, 24, 4>();
-    benchp<30, 26, 4>();
-    bench2<30, 22, 4, 1024>(1);
-    bench2<30, 23, 5, 1024>(1);
+    for (int rep = 0; rep < 2; ++rep) {
+        bench3<false, false, 1024>();
+        bench3<false, true, 1024>();
+        bench3<false, false, 1024, true>();
+        bench3<false, true, 1024, true>();
+        bench3<false, true, 512>();
+        bench3<false, true, 512, true>();
+        bench3<false, false, 512, true>();
+    }
     return 0;
 }
