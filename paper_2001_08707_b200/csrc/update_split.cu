@@ -107,12 +107,36 @@ struct SplitSeed {
     cplx red8[8];
 };
 
+// Per-thread view of the H_B bonds of the rows e = tid | (k << NB) (k < PER, NT = 2^NB threads):
+// a bond between two local bits is decided by tid alone (both bits < NB: a per-thread constant),
+// by tid and k (one bit each), or by k alone (a compile-time constant once k is unrolled); its
+// partner index is e ^ (bit mask) = (tid ^ low mask) | ((k ^ high mask) << NB).  Precomputing the
+// per-thread parts turns every partner read into one LDS at a per-thread base + an immediate
+// (ncu: the generic bit tests and index arithmetic were ~75 of 184 instructions per row).
+template <int HB, int TB, int NB>
+struct BondView {
+    static constexpr int PB = TB - HB, NBOND = HB;   // HB - 1 chain bonds + the periodic one
+    int lo_bit1[NBOND], lo_bit2[NBOND];              // tid's bits at the bond's two local bits
+    __device__ __forceinline__ static constexpr int b1(int j) { return j < HB - 1 ? PB + j : TB - 1; }
+    __device__ __forceinline__ static constexpr int b2(int j) { return j < HB - 1 ? PB + j + 1 : 0; }
+    __device__ __forceinline__ static constexpr int mask(int j) { return (1 << b1(j)) | (1 << b2(j)); }
+    // bit `b` of e = tid | (k << NB)
+    __device__ __forceinline__ static int bit(int tid, int k, int b) {
+        return b < NB ? (tid >> b) & 1 : (k >> (b - NB)) & 1;
+    }
+};
+
 template <int HB, int TB, int NT>
 __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const cplx *__restrict__ q) {
-    constexpr int TS = 1 << TB, PER = TS / NT;
-    static_assert(PER * NT == TS && NT >= 256, "B-tile must be a multiple of the CTA");
-    extern __shared__ __align__(16) cplx S2[];   // [2][TS] staged r_n, then r_{n+1}
-    __shared__ ShiftScratch ss;
+    constexpr int TS = 1 << TB, PER = TS / NT, PB = TB - HB;
+    constexpr int NB = NT == 256 ? 8 : NT == 512 ? 9 : 10;
+    static_assert((1 << NB) == NT && PER * NT == TS && NT % (1 << PB) == 0, "CTA / B-tile / piece shape");
+    using BV = BondView<HB, TB, NB>;
+    // [2][TS]: r_n of the tile (cp.async staging) and r_{n+1} of the tile.  Shared memory is kept
+    // to 128 KB + a few KB so ~95 KB of L1 remain for the row-stream loads in flight (with a
+    // third 64-KB buffer the update ran 16 -> 22 ms: the loads had no L1 to land in).  The shift
+    // agents' scratch lives in the same dynamic region (agents do not stream).
+    extern __shared__ __align__(16) cplx S3[];
     __shared__ SplitSeed us;
     __shared__ cplx scratch[4 * (NT / 32)];
     pdl_wait();
@@ -125,9 +149,19 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
     const cplx *__restrict__ rc_ = pick3(kp.r, ns + 2);   // r_n
     const cplx *__restrict__ rp_ = pick3(kp.r, ns + 1);   // r_{n-1}
     cplx *__restrict__ rn_ = pick3(kp.r, ns);             // r_{n+1}
+    // tid < NT explicit (e = tid | (k << NB)); row of e in B-tile t: row0 + k kstep + (t << PB)
+    const int tid = threadIdx.x & (NT - 1);
+    const int64_t row0 = split_row<HB, TB>(0, tid, ahi);
+    const int64_t kstep = (int64_t)(NT >> PB) << ahi;
+    cplx *const S = S3, *const W = S3 + TS;   // r_n, r_{n+1} of the current tile
+    auto stage = [&](int64_t t) {
+        const cplx *src = rc_ + row0 + (t << PB);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) cp_async16(S + (tid | (k << NB)), src + k * kstep);
+        cp_async_commit();
+    };
     // the first tile's r_n does not depend on the seed scalars: in flight during the w reduction
-    if (wb >= 0 && wb < ntiles) stage_tile<HB, TB, NT>(S2, rc_, wb, ahi);
-    cp_async_commit();
+    if (wb >= 0 && wb < ntiles) stage(wb);
     // ---- seed step (a3): w = w_A + w_B partials of this iteration's half, fixed order
     {
         const int64_t m = st->n_started;
@@ -149,24 +183,15 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
         }
     }
     if (blockIdx.x < kp.n_agents) {   // shift agents (a4 + a6 + pending a8)
-        shift_step(kp, ss, blockIdx.x, us.o.alpha, us.o.beta, us.o.c);
+        static_assert(sizeof(ShiftScratch) <= 2 * TS * sizeof(cplx), "agent scratch fits the tile buffers");
+        shift_step(kp, *reinterpret_cast<ShiftScratch *>(S3), blockIdx.x, us.o.alpha, us.o.beta, us.o.c);
         return;
     }
     const cplx a_cur = us.o.a_cur, a_q = us.o.a_q, a_prev = us.o.a_prev;
     const double hJ = 0.5 * kp.J;
     const cplx *__restrict__ left = kp.left;
     cplx rho = mk(0.0, 0.0), nu = mk(0.0, 0.0), g = mk(0.0, 0.0), wbp = mk(0.0, 0.0);
-    // row of local index e = tid + k NT in B-tile t: row0 + k kstep + (t << PB) (NT is a multiple
-    // of the piece, so k moves whole pieces: (NT >> PB) high-bit steps of 2^AHI rows)
-    constexpr int PB = TB - HB;
-    static_assert(NT % (1 << PB) == 0, "a thread's rows sit at the same offset in their pieces");
-    const int64_t row0 = split_row<HB, TB>(0, threadIdx.x, ahi);
-    const int64_t kstep = (int64_t)(NT >> PB) << ahi;
-    int it = 0;
-    for (int64_t t = wb; t < ntiles; t += nwb, ++it) {
-        cplx *S = S2 + (it & 1) * TS;
-        if (t + nwb < ntiles) stage_tile<HB, TB, NT>(S2 + ((it + 1) & 1) * TS, rc_, t + nwb, ahi);
-        cp_async_commit();
+    for (int64_t t = wb; t < ntiles; t += nwb) {
         // every row-stream load of the tile is issued before waiting for its staged r_n (they do
         // not depend on it): 3 PER loads in flight per thread across the wait and the barrier
         const int64_t rt = row0 + (t << PB);
@@ -178,30 +203,48 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
             rp[k] = ldg_cs(rp_ + s);
             lv[k] = ldg_cs(left + s);
         }
-        cp_async_wait<1>();   // this tile's r_n has landed (the next one stays in flight)
-        __syncthreads();
-        cplx o[PER];
+        cp_async_wait<0>();   // this tile's r_n has landed (staged during the previous w_B pass)
+        __syncthreads();      // ... for every thread; and W of the previous tile is consumed
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const int e = threadIdx.x + k * NT;
-            const cplx h = hb_partners<HB, TB>(S, e);
+            const int e = tid | (k << NB);
+            cplx h = mk(0.0, 0.0);   // (H_B r_n)_e / (J/2): anti-aligned bonds' partners
+#pragma unroll
+            for (int j = 0; j < BV::NBOND; ++j) {
+                if (BV::bit(tid, k, BV::b1(j)) != BV::bit(tid, k, BV::b2(j))) {
+                    const cplx p = S[e ^ BV::mask(j)];
+                    h.x += p.x;
+                    h.y += p.y;
+                }
+            }
             const cplx qf = mk(fma(hJ, h.x, qa[k].x), fma(hJ, h.y, qa[k].y));   // (H r_n)_s
             cplx rn = cmul(a_cur, S[e]);
             rn = cfma(a_q, qf, rn);
             rn = cfma(a_prev, rp[k], rn);
             rn_[rt + k * kstep] = rn;
+            W[e] = rn;
             rho = cfma(rn, rn, rho);
             nu.x = fma(rn.x, rn.x, fma(rn.y, rn.y, nu.x));
             g = cfma_conj(lv[k], rn, g);
-            o[k] = rn;
         }
-        __syncthreads();   // every H_B read of r_n is done: park r_{n+1} in its place
+        __syncthreads();   // r_{n+1} of the tile complete in W; r_n no longer read
+        if (t + nwb < ntiles) stage(t + nwb);   // in flight during the w_B pass
 #pragma unroll
-        for (int k = 0; k < PER; ++k) S[threadIdx.x + k * NT] = o[k];
-        __syncthreads();
+        for (int k = 0; k < PER; ++k) {   // w_B: each anti-aligned pair once (lower bit 0, upper 1)
+            const int e = tid | (k << NB);
+            cplx h = mk(0.0, 0.0);
 #pragma unroll
-        for (int k = 0; k < PER; ++k) wbp = cadd(wbp, hb_pairs<HB, TB>(S, threadIdx.x + k * NT, o[k]));
-        __syncthreads();   // this buffer is refilled two tiles later
+            for (int j = 0; j < BV::NBOND; ++j) {
+                // chain bond: lower bit b1, upper b2; periodic: lower bit 0 (= b2), upper L-1 (= b1)
+                const int lower = j < HB - 1 ? BV::b1(j) : BV::b2(j), upper = j < HB - 1 ? BV::b2(j) : BV::b1(j);
+                if (!BV::bit(tid, k, lower) && BV::bit(tid, k, upper)) {
+                    const cplx p = W[e ^ BV::mask(j)];
+                    h.x += p.x;
+                    h.y += p.y;
+                }
+            }
+            wbp = cfma(W[e], h, wbp);
+        }
     }
     // CTA partials: rho, ||r||^2, a^dag r (part_u) and w_B (the next half of part_w)
     wbp = mk(2.0 * hJ * wbp.x, 2.0 * hJ * wbp.y);
@@ -257,18 +300,21 @@ int split_ahi_for(int L, int64_t M, int world, int bicg, int full, int nl, int k
     return (en == 1 || L >= 24) ? ahi : 0;
 }
 
-int split_blocks() { return sm_count(); }   // one CTA per SM (128 KB of staging each)
+int split_blocks() { return sm_count(); }   // one CTA per SM (128 KB of shared memory each)
 
-static size_t split_smem() { return 2 * (sizeof(cplx) << kSplitTB); }
+// dynamic shared memory: the update stages r_n in one buffer and parks r_{n+1} in a second; the
+// init kernel uses one
+static size_t split_smem_update() { return 2 * (sizeof(cplx) << kSplitTB); }
+static size_t split_smem_init() { return sizeof(cplx) << kSplitTB; }
 
 static cudaError_t split_setup() {
     static PerDevice once;
     return once_per_device(once, [] {
         cudaError_t e = cudaFuncSetAttribute(update_split_kernel<kSplitHB, kSplitTB, kSplitNT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem());
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem_update());
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(split_wb_kernel<kSplitHB, kSplitTB, kSplitNT>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem());
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem_init());
         return e;
     });
 }
@@ -277,13 +323,13 @@ cudaError_t launch_update_split(const KParams &kp, const cplx *q, cudaStream_t s
     const cudaError_t e = split_setup();
     if (e != cudaSuccess) return e;
     return launch_k(update_split_kernel<kSplitHB, kSplitTB, kSplitNT>, kp.nblk_upd + kp.n_agents, kSplitNT,
-                    split_smem(), s, true, kp, q);
+                    split_smem_update(), s, true, kp, q);
 }
 
 cudaError_t launch_split_init(const KParams &kp, cudaStream_t s) {
     const cudaError_t e = split_setup();
     if (e != cudaSuccess) return e;
-    split_wb_kernel<kSplitHB, kSplitTB, kSplitNT><<<kp.nblk_upd, kSplitNT, split_smem(), s>>>(
+    split_wb_kernel<kSplitHB, kSplitTB, kSplitNT><<<kp.nblk_upd, kSplitNT, split_smem_init(), s>>>(
         kp, kp.r[0], kp.part_w + kp.wsplit_off);
     return cudaGetLastError();
 }
