@@ -305,6 +305,11 @@ int sk_checkpoint(sk_ctx *ctx, void *buf, size_t *bytes);
 int sk_restore(sk_ctx *ctx, const void *buf, size_t bytes);
 
 /* ---- multi-rank setup (see sk_dist) ---- */
+/* Host all-reduce supplied by the caller (MPI_Allreduce, a gloo/torch.distributed group, ...):
+   sum `n` doubles of `send` over the ranks into `recv` (both HOST memory owned by the library,
+   valid for the call only); every rank must receive bit-identical sums.  Returns 0 on success. */
+typedef int (*sk_allreduce_fn)(void *user, const double *send, double *recv, int64_t n);
+
 /* CUDA IPC handle (64 bytes) of this context's device arena, for the other ranks. */
 int sk_ipc_handle(sk_ctx *ctx, void *out64);
 /* A fresh ncclUniqueId (128 bytes); call on one rank and broadcast. */
@@ -312,6 +317,15 @@ int sk_nccl_unique_id(void *out128);
 /* Map every other rank's arena (handles: [world][64] from sk_ipc_handle, in rank order), join
    the NCCL communicator and finish the initialisation (global rho_0, ||b||, P b).  Collective. */
 int sk_connect(sk_ctx *ctx, const void *handles, const void *nccl_id);
+/* As sk_connect, but the two small all-reduces of every iteration (w; then rho, ||r||^2, P r —
+   P:L973's parallel products) go through `fn` on the host instead of NCCL: the
+   library copies this rank's partials to host, calls fn, copies the sums back (the stream is
+   synchronised around the call, so iterations run without graph capture).  The operator's
+   off-rank reads still go through the mapped peer arenas inside the SpMV kernels.  No kernel of
+   one rank ever waits on another rank's kernel: ranks meet only inside fn.  For MPI codes (the
+   paper's own parallelisation) and for testing the IPC data plane with several processes
+   on one GPU.  Collective. */
+int sk_connect_host(sk_ctx *ctx, const void *handles, sk_allreduce_fn fn, void *user);
 /* Loopback group of `world` virtual ranks on one device (all share one stream). */
 int sk_group_create(sk_group **out, int32_t world, int32_t device);
 /* After sk_init of every rank with this group: wire the ranks and finish initialisation. */

@@ -120,6 +120,9 @@ struct sk_ctx {
     size_t arena_bytes = 0;
     double b_norm = 0;              // ||b|| (global), recorded at initialisation
     std::vector<void *> peer_bases; // opened IPC mappings of the other ranks' arenas
+    sk_allreduce_fn host_ar = nullptr;   // host all-reduce (sk_connect_host) instead of NCCL
+    void *host_ar_user = nullptr;
+    double *host_stage = nullptr;        // pinned [2][2 (2 + nl)] doubles: send, recv
 };
 
 static cudaError_t prof_mark(sk_ctx *c) {
@@ -158,6 +161,7 @@ static void destroy(sk_ctx *c) {
     if (c->group && c->rank < (int)c->group->members.size()) c->group->members[c->rank] = nullptr;
     for (void *p : c->allocs) cudaFree(p);
     if (c->st_host) cudaFreeHost(c->st_host);
+    if (c->host_stage) cudaFreeHost(c->host_stage);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -204,6 +208,16 @@ static int enqueue_phase_b(sk_ctx *c, const sk::SpmvArgs &a) {
 }
 
 static int nccl_allreduce(sk_ctx *c, const cplx *src, cplx *dst, int ncplx) {
+    if (c->host_ar) {   // sk_connect_host: through the caller's host collective
+        const int64_t n = 2 * (int64_t)ncplx;
+        double *snd = c->host_stage, *rcv = c->host_stage + n;
+        CK(cudaMemcpyAsync(snd, src, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->host_ar(c->host_ar_user, snd, rcv, n) != 0) return fail(SK_ENCCL, "host all-reduce callback failed");
+        CK(cudaMemcpyAsync(dst, rcv, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));   // (the staging buffer is reused by the next call)
+        return SK_OK;
+    }
     NK(nccl().allReduce(src, dst, 2 * (size_t)ncplx, ncclDouble, ncclSum, c->comm, c->stream));
     return SK_OK;
 }
@@ -684,10 +698,7 @@ int sk_nccl_unique_id(void *out128) {
     return SK_OK;
 }
 
-int sk_connect(sk_ctx *c, const void *handles, const void *nccl_id) {
-    if (!c || !handles || !nccl_id) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
-    if (c->world == 1 || c->group || c->connected) return fail(SK_ESTATE, "not an unconnected NCCL-mode context");
-    if (!nccl().ok) return fail(SK_ENCCL, "libnccl.so.2 not loadable");
+static int map_peers(sk_ctx *c, const void *handles) {
     CK(cudaSetDevice(c->device));
     std::vector<char *> bases(c->world);
     c->peer_bases.assign(c->world, nullptr);
@@ -700,11 +711,31 @@ int sk_connect(sk_ctx *c, const void *handles, const void *nccl_id) {
         c->peer_bases[g] = p;
         bases[g] = (char *)p;
     }
+    return write_shard_tables(c, bases);
+}
+
+int sk_connect(sk_ctx *c, const void *handles, const void *nccl_id) {
+    if (!c || !handles || !nccl_id) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (c->world == 1 || c->group || c->connected) return fail(SK_ESTATE, "not an unconnected NCCL-mode context");
+    if (!nccl().ok) return fail(SK_ENCCL, "libnccl.so.2 not loadable");
     int rc;
-    if ((rc = write_shard_tables(c, bases)) != SK_OK) return rc;
+    if ((rc = map_peers(c, handles)) != SK_OK) return rc;
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof(id));
     NK(nccl().commInitRank(&c->comm, c->world, id, c->rank));
+    if ((rc = nccl_allreduce(c, c->kp.uloc, c->kp.usum, 2 + c->nl)) != SK_OK) return rc;
+    return finish_init(c);
+}
+
+int sk_connect_host(sk_ctx *c, const void *handles, sk_allreduce_fn fn, void *user) {
+    if (!c || !handles || !fn) return fail(c ? SK_EINVAL : SK_ESTATE, "null argument");
+    if (c->world == 1 || c->group || c->connected) return fail(SK_ESTATE, "not an unconnected multi-rank context");
+    int rc;
+    if ((rc = map_peers(c, handles)) != SK_OK) return rc;
+    if (cudaMallocHost((void **)&c->host_stage, sizeof(double) * 4 * (2 + c->nl)) != cudaSuccess)
+        return fail(SK_ENOMEM, "cudaMallocHost (all-reduce staging)");
+    c->host_ar = fn;
+    c->host_ar_user = user;
     if ((rc = nccl_allreduce(c, c->kp.uloc, c->kp.usum, 2 + c->nl)) != SK_OK) return rc;
     return finish_init(c);
 }
@@ -859,7 +890,7 @@ static int capture_graph(sk_ctx *c, int iters) {
 // remainders are rare and should not pay a second capture).
 static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk, bool single1 = false) {
     int rc;
-    if (c->profiling) chunk = 1;   // individual launches bracketed by events
+    if (c->profiling || c->host_ar) chunk = 1;   // individual launches (events; host collectives)
     if (iters >= chunk && chunk > 1) {
         if ((rc = capture_graph(c, chunk)) != SK_OK) return rc;
     }

@@ -90,6 +90,23 @@ def connect(solver, pg=None):
     solver.connect(handles, nid)
 
 
+def connect_host(solver, pg=None):
+    """Connection with the host collective of a torch.distributed group (e.g. gloo) in place of
+    NCCL (sk_connect_host): IPC handles all-gathered through `pg`, the per-iteration all-reduces
+    of the dots through `pg` on the host.  Several processes may share one GPU this way (no
+    kernel waits on another process's kernel)."""
+    import torch
+    import torch.distributed as dist
+    allh = [None] * dist.get_world_size(pg)
+    dist.all_gather_object(allh, solver.ipc_handle(), group=pg)
+
+    def allreduce(send, recv):
+        t = torch.from_numpy(send.copy())
+        dist.all_reduce(t, group=pg)
+        recv[:] = t.numpy()
+    solver.connect_host(b"".join(allh), allreduce)
+
+
 def remote_rows_per_spmv(problem, world: int, rank: int) -> int:
     """Rows of OTHER ranks this rank's SpMV reads per application (each a 16-B complex128 read
     over NVLink; element count, the algorithmic exchange volume of SURVEY §8(e)).

@@ -32,7 +32,7 @@ EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_ru
            "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
            "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
            "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc", "sk_checkpoint",
-           "sk_restore", "sk_combine", "sk_gram", "sk_get_info"]
+           "sk_restore", "sk_combine", "sk_gram", "sk_get_info", "sk_connect_host"]
 
 
 class ShiftkError(RuntimeError):
@@ -87,6 +87,10 @@ class sk_profile(ctypes.Structure):
 
 _lib = None
 
+# sk_allreduce_fn: int (*)(void *user, const double *send, double *recv, int64_t n)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+
 
 def load(path: str = LIB_PATH):
     """Load libshiftk.so (no fallback: raises if it is missing)."""
@@ -129,6 +133,7 @@ def load(path: str = LIB_PATH):
         "sk_restore": [VP, VP, ctypes.c_size_t],
         "sk_get_profile": [VP, P(sk_profile), I32],
         "sk_get_info": [VP, P(sk_info)],
+        "sk_connect_host": [VP, VP, ALLREDUCE_FN, VP],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -308,6 +313,21 @@ class Solver:
 
     def connect(self, handles: bytes, nccl_id: bytes):
         _check(load().sk_connect(self._h, handles, nccl_id), "sk_connect")
+
+    def connect_host(self, handles: bytes, allreduce):
+        """sk_connect_host: `allreduce(send: np.ndarray, recv: np.ndarray)` sums `send` (float64,
+        host) over the ranks into `recv` (marshalling only: the arithmetic of the method stays
+        in the kernels; this is the collective the caller owns, e.g. MPI or gloo)."""
+        import numpy as _np
+
+        def cb(user, send, recv, n):
+            try:
+                allreduce(_np.ctypeslib.as_array(send, shape=(n,)), _np.ctypeslib.as_array(recv, shape=(n,)))
+                return 0
+            except Exception:   # reported to the library as a failed collective (SK_ENCCL)
+                return 1
+        self._allreduce_cb = ALLREDUCE_FN(cb)   # kept alive as long as the context
+        _check(load().sk_connect_host(self._h, handles, self._allreduce_cb, None), "sk_connect_host")
 
     # -- iteration ---------------------------------------------------------------------
     def update(self) -> int:
