@@ -300,6 +300,67 @@ def config_dict(problem, world):
     return c
 
 
+# ------------------------------------------------------------------------------ whole convergence
+
+def run_converge(args, problem):
+    """SURVEY §8(d.5) for C1/C2: the WHOLE convergence run (sk_run with status polled every 256
+    iterations, graph-captured) timed with CUDA events on the solver's stream, median of
+    `--repeats` runs on fresh contexts; one-time costs (module load, graph capture) are paid by a
+    warm-up context first.  The OpenMP oracle's own full run beside it."""
+    import torch
+    from paper_2001_08707_b200 import shiftk
+    from paper_2001_08707_b200.device import to_device
+    dp = to_device(problem)
+    st = torch.cuda.Stream()
+    mk = lambda: shiftk.Solver(dp.op, problem.method, dp.b, problem.z, left=dp.left,
+                               full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax,
+                               stream=st.cuda_stream)
+    w = mk()
+    w.run(256, poll_every=256)
+    w.finalize()
+    runs = []
+    with ClockSampler(0) as clk:
+        for _ in range(max(1, args.repeats)):
+            s = mk()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(st):
+                a.record(st)
+                status = s.run(problem.itermax, poll_every=256)
+                b.record(st)
+            torch.cuda.synchronize()
+            c = s.coefficients()
+            _, _, ret = s.shift_state()
+            runs.append((a.elapsed_time(b), status, c, ret, s.residuals()))
+            s.finalize()
+    runs.sort(key=lambda r: r[0])
+    ms, status, c, ret, res = runs[len(runs) // 2]
+    its = c["iterations"]
+    line = {"metric": METRIC, "value": problem.n_shift * its / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+            "steps": its, "warmup": 256, "ms_per_step": ms / its, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": dict(config_dict(problem, 1), l2="not flushed (one continuous run)"),
+            "mode": "whole convergence (SURVEY 8(d.5))",
+            "converge": {"status": shiftk.STATUS_NAMES[status], "iterations": its, "switches": c["switches"],
+                         "total_ms": ms, "runs_ms": [r[0] for r in runs],
+                         "active_shift_iterations": int(sum(int(r) if r >= 0 else its for r in ret)),
+                         "max_residual": float(np.max(res)), "tol": problem.tol},
+            "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        import oracle
+        o = oracle.Oracle(problem.method, problem.b, problem.z, left=problem.left,
+                          full_x=problem.full_x, tol=problem.tol, itermax=problem.itermax, omp=True)
+        t0 = time.perf_counter()
+        ost = o.run(problem.op, problem.itermax)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": problem.n_shift * o.iterations / dt, "unit": UNIT,
+                                "cores": oracle.threads(), "kind": "oracle", "host": host_info(),
+                                "sample": f"the oracle's whole run of {problem.name}: {o.iterations} iterations "
+                                          f"({oracle.STATUS_NAMES[ost]}) in {dt:.1f} s on {oracle.threads()} threads"}
+        o.close()
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------------------ GPU leg
 
 def main():
@@ -313,6 +374,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=3, help="timed passes (value = the median)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--converge", action="store_true", help="time the whole convergence run (C1, C2)")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
     rank, world, local = dist_env()
@@ -320,6 +382,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, problem)
+        return
+    if args.converge:
+        run_converge(args, problem)
         return
 
     import torch

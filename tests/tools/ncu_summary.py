@@ -44,7 +44,9 @@ def full(rep):
                 "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
                 "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
                 "launch__grid_size", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second",
-                "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+                "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "lts__t_sectors_srcunit_tex_op_read.sum", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                "lts__t_sectors.avg.pct_of_peak_sustained_elapsed"]
         e = {k: (d.get(k), units[hdr.index(k)] if k in hdr else None) for k in keys}
         e["top_stalls_pct"] = {w: round(100 * v / tot, 1) for v, w in sorted(stalls, reverse=True)[:6]}
         res.append(e)
