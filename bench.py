@@ -100,6 +100,8 @@ class ClockSampler:
         self.nvml = None
         self.lines = []
         self.samples = []     # (sm_mhz, sm_max_mhz, {reason names}) from NVML
+        self.power = []       # board power samples (W), NVML
+        self.power_limit = None
         self.stop = threading.Event()
         self.source = None
 
@@ -138,6 +140,12 @@ class ClockSampler:
         sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         self.samples.append((sm, self.smax, {n for n, b in zip(self.NAMES, self.bits) if r & b}))
+        try:   # board power (W), to explain sw_power_cap (the enforced limit is recorded once)
+            self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+            if self.power_limit is None:
+                self.power_limit = nv.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+        except Exception:
+            pass
 
     def _poll(self):
         while not self.stop.wait(self.period):
@@ -184,6 +192,8 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "power_w": statistics.median(self.power) if self.power else None,
+                "power_limit_w": self.power_limit,
                 "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 

@@ -404,7 +404,10 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
                    : H->kind == SK_OP_HEISENBERG_SZ ? sk::sz_blocks(H->L, M, kp.bicg)
                    : H->kind == SK_OP_RC ? sk::stream_blocks(M) : sk::csr_blocks(M);
     kp.nblk_upd = sk::update_blocks(M, c->nl, c->full, c->nz);
-    if (kp.split_ahi) kp.nblk_upd = sk::split_blocks();
+    if (kp.split_ahi) {
+        kp.nblk_upd = sk::split_blocks();
+        kp.split_lo = sk::split_lo_bonds();
+    }
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
     kp.rank = rank;

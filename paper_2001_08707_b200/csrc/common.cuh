@@ -159,7 +159,7 @@ struct KParams {
     // and the partials of w_B = <r, H_B r> of the r it writes, at [wsplit_off, + nblk_upd) of
     // the next half of part_w (inside the range the seed step reduces).  split_ahi = 0: off.
     int32_t split_ahi;
-    int32_t pad_split_;
+    int32_t split_lo;            // bonds (i, i+1), i < split_lo, are in H_B too (B-tile piece bits)
     int64_t wsplit_off;
     double J;                    // exchange coupling of the Heisenberg operator (H_B amplitudes)
     // per-shift arrays [nz]

@@ -114,6 +114,7 @@ cudaError_t launch_update(const KParams &kp, const cplx *q, const cplx *qt, cuda
 // applies H_B and writes the w_B partials; launch_split_init writes those of r_0.
 int split_ahi_for(int L, int64_t M, int world, int bicg, int full, int nl, int kind_heisenberg);
 int split_blocks();
+int split_lo_bonds();   // in-piece bonds (0,1).. moved from H_A to H_B (0: none)
 cudaError_t launch_update_split(const KParams &kp, const cplx *q, cudaStream_t s);
 cudaError_t launch_split_init(const KParams &kp, cudaStream_t s);
 

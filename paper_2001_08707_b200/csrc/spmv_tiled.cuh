@@ -162,6 +162,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
             const unsigned xt = (unsigned)(tid ^ (tid >> 1));
 #pragma unroll
             for (int i = 0; i < 7; ++i) {
+                if (SPLIT && i < kp.split_lo) continue;   // in H_B (the update's B-tiles, §5.9)
                 if ((xt >> i) & 1u) {
                     const int lp = tid ^ (3 << i);
 #pragma unroll

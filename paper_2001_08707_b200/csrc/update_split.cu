@@ -46,48 +46,6 @@ static __device__ __forceinline__ int64_t split_row(int64_t t, int e, int ahi) {
     return ((int64_t)(e >> PB) << ahi) | (t << PB) | (int64_t)(e & ((1 << PB) - 1));
 }
 
-// sum of the H_B partners of local row e (bond (AHI+j, AHI+j+1) <-> local bits PB+j, PB+j+1;
-// periodic (L-1, 0) <-> local bits TB-1, 0): every anti-aligned bond contributes r[e ^ flip]
-template <int HB, int TB>
-static __device__ __forceinline__ cplx hb_partners(const cplx *S, int e) {
-    constexpr int PB = TB - HB;
-    cplx h = mk(0.0, 0.0);
-#pragma unroll
-    for (int j = 0; j < HB - 1; ++j)
-        if (((e >> (PB + j)) ^ (e >> (PB + j + 1))) & 1) {
-            const cplx p = S[e ^ (3 << (PB + j))];
-            h.x += p.x;
-            h.y += p.y;
-        }
-    if (((e >> (TB - 1)) ^ e) & 1) {
-        const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
-        h.x += p.x;
-        h.y += p.y;
-    }
-    return h;
-}
-
-// Each anti-aligned pair of H_B once (from the row whose lower bond bit is 0): the pair's two
-// terms r_e r_p J/2 + r_p r_e J/2 of <r, H_B r> are added as one product (caller doubles).
-template <int HB, int TB>
-static __device__ __forceinline__ cplx hb_pairs(const cplx *S, int e, cplx re) {
-    constexpr int PB = TB - HB;
-    cplx h = mk(0.0, 0.0);
-#pragma unroll
-    for (int j = 0; j < HB - 1; ++j)
-        if (!((e >> (PB + j)) & 1) && ((e >> (PB + j + 1)) & 1)) {
-            const cplx p = S[e ^ (3 << (PB + j))];
-            h.x += p.x;
-            h.y += p.y;
-        }
-    if (!(e & 1) && ((e >> (TB - 1)) & 1)) {
-        const cplx p = S[e ^ ((1 << (TB - 1)) | 1)];
-        h.x += p.x;
-        h.y += p.y;
-    }
-    return cmul(re, h);
-}
-
 template <int HB, int TB, int NT>
 static __device__ __forceinline__ void stage_tile(cplx *S, const cplx *__restrict__ r, int64_t t, int ahi) {
     constexpr int TS = 1 << TB;
@@ -115,11 +73,20 @@ struct SplitSeed {
 // (ncu: the generic bit tests and index arithmetic were ~75 of 184 instructions per row).
 template <int HB, int TB, int NB>
 struct BondView {
-    static constexpr int PB = TB - HB, NBOND = HB;   // HB - 1 chain bonds + the periodic one
-    int lo_bit1[NBOND], lo_bit2[NBOND];              // tid's bits at the bond's two local bits
-    __device__ __forceinline__ static constexpr int b1(int j) { return j < HB - 1 ? PB + j : TB - 1; }
-    __device__ __forceinline__ static constexpr int b2(int j) { return j < HB - 1 ? PB + j + 1 : 0; }
+    // bonds of H_B in local bits: j < NPIECE: (j, j+1) inside the piece (moved from H_A when
+    // kp.split_lo = NPIECE, §5.9); then the chain (PB+i, PB+i+1), i < HB-1; last the periodic
+    // (TB-1, 0).  For the pair count of w_B, `lower` is the bond's lower spin site.
+    static constexpr int PB = TB - HB, NPIECE = PB - 1, NBOND = NPIECE + HB;
+    __device__ __forceinline__ static constexpr int b1(int j) {
+        return j < NPIECE ? j : (j < NBOND - 1 ? PB + (j - NPIECE) : TB - 1);
+    }
+    __device__ __forceinline__ static constexpr int b2(int j) {
+        return j < NPIECE ? j + 1 : (j < NBOND - 1 ? PB + (j - NPIECE) + 1 : 0);
+    }
+    __device__ __forceinline__ static constexpr int lower(int j) { return j < NBOND - 1 ? b1(j) : b2(j); }
+    __device__ __forceinline__ static constexpr int upper(int j) { return j < NBOND - 1 ? b2(j) : b1(j); }
     __device__ __forceinline__ static constexpr int mask(int j) { return (1 << b1(j)) | (1 << b2(j)); }
+    __device__ __forceinline__ static constexpr bool piece(int j) { return j < NPIECE; }
     // bit `b` of e = tid | (k << NB)
     __device__ __forceinline__ static int bit(int tid, int k, int b) {
         return b < NB ? (tid >> b) & 1 : (k >> (b - NB)) & 1;
@@ -190,6 +157,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
     const cplx a_cur = us.o.a_cur, a_q = us.o.a_q, a_prev = us.o.a_prev;
     const double hJ = 0.5 * kp.J;
     const cplx *__restrict__ left = kp.left;
+    const bool lo = kp.split_lo != 0;   // the piece bonds (0,1)..(PB-2,PB-1) are in H_B
     cplx rho = mk(0.0, 0.0), nu = mk(0.0, 0.0), g = mk(0.0, 0.0), wbp = mk(0.0, 0.0);
     for (int64_t t = wb; t < ntiles; t += nwb) {
         // every row-stream load of the tile is issued before waiting for its staged r_n (they do
@@ -211,7 +179,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
             cplx h = mk(0.0, 0.0);   // (H_B r_n)_e / (J/2): anti-aligned bonds' partners
 #pragma unroll
             for (int j = 0; j < BV::NBOND; ++j) {
-                if (BV::bit(tid, k, BV::b1(j)) != BV::bit(tid, k, BV::b2(j))) {
+                if ((!BV::piece(j) || lo) && BV::bit(tid, k, BV::b1(j)) != BV::bit(tid, k, BV::b2(j))) {
                     const cplx p = S[e ^ BV::mask(j)];
                     h.x += p.x;
                     h.y += p.y;
@@ -235,9 +203,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
             cplx h = mk(0.0, 0.0);
 #pragma unroll
             for (int j = 0; j < BV::NBOND; ++j) {
-                // chain bond: lower bit b1, upper b2; periodic: lower bit 0 (= b2), upper L-1 (= b1)
-                const int lower = j < HB - 1 ? BV::b1(j) : BV::b2(j), upper = j < HB - 1 ? BV::b2(j) : BV::b1(j);
-                if (!BV::bit(tid, k, lower) && BV::bit(tid, k, upper)) {
+                if ((!BV::piece(j) || lo) && !BV::bit(tid, k, BV::lower(j)) && BV::bit(tid, k, BV::upper(j))) {
                     const cplx p = W[e ^ BV::mask(j)];
                     h.x += p.x;
                     h.y += p.y;
@@ -274,10 +240,22 @@ __global__ void __launch_bounds__(NT, 1) split_wb_kernel(KParams kp, const cplx 
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
+        constexpr int NB = NT == 256 ? 8 : NT == 512 ? 9 : 10;
+        using BV = BondView<HB, TB, NB>;
+        const int tid = threadIdx.x & (NT - 1);
+        const bool lo = kp.split_lo != 0;
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int e = threadIdx.x + k * NT;
-            wbp = cadd(wbp, hb_pairs<HB, TB>(S2, e, S2[e]));
+        for (int k = 0; k < PER; ++k) {   // as the update's w_B pass
+            const int e = tid | (k << NB);
+            cplx h = mk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < BV::NBOND; ++j)
+                if ((!BV::piece(j) || lo) && !BV::bit(tid, k, BV::lower(j)) && BV::bit(tid, k, BV::upper(j))) {
+                    const cplx p = S2[e ^ BV::mask(j)];
+                    h.x += p.x;
+                    h.y += p.y;
+                }
+            wbp = cfma(S2[e], h, wbp);
         }
         __syncthreads();
     }
@@ -298,6 +276,18 @@ int split_ahi_for(int L, int64_t M, int world, int bicg, int full, int nl, int k
     const int ahi = L - kSplitHB;
     if (ahi < kTileBits || ahi < kSplitTB - kSplitHB || M != (int64_t(1) << L) || L > 31) return 0;
     return (en == 1 || L >= 24) ? ahi : 0;
+}
+
+// SHIFTK_SPLIT_LO=1 moves the piece bonds (0,1)..(PB-2,PB-1) from H_A (the SpMV) to H_B (the
+// update).  Measured at C5: SpMV 10.5 -> 9.8 ms, update 15.3 -> 17.2 ms (the update's predicated
+// bond loads: 4.4e9 -> 5.9e9 instructions) — so off by default.
+int split_lo_bonds() {
+    static int lo = -1;
+    if (lo < 0) {
+        const char *e = getenv("SHIFTK_SPLIT_LO");
+        lo = (e && e[0] == '1') ? kSplitTB - kSplitHB - 1 : 0;
+    }
+    return lo;
 }
 
 int split_blocks() { return sm_count(); }   // one CTA per SM (128 KB of shared memory each)

@@ -363,14 +363,17 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("a_kernel", ["stream", "tiled"])
+@pytest.mark.parametrize("a_kernel", ["stream", "tiled", "tiled-lo"])
 def test_bond_split_forced_at_small_l(a_kernel):
     """The bond split forced at L = 20, 21, 22 (SHIFTK_HEIS_SPLIT=1; H_A by the streaming SpMV
     (SHIFTK_HEIS_STREAM=1, per-tile w partials) or the tiled one (per-CTA partials); AHI =
     12..14, so the B-tiles cover 7 chain bonds + the periodic one and 2^8..2^10 B-tiles over 148
     CTAs): 40-iteration oracle windows on 64 shifts, graph == stepwise bitwise, restart from a
     checkpoint against the oracle, and a converged run."""
-    _subprocess(SPLIT_FORCED, {"SHIFTK_HEIS_SPLIT": "1", "SHIFTK_HEIS_STREAM": "1" if a_kernel == "stream" else "0"})
+    env = {"SHIFTK_HEIS_SPLIT": "1", "SHIFTK_HEIS_STREAM": "1" if a_kernel == "stream" else "0"}
+    if a_kernel == "tiled-lo":   # the piece bonds (0,1)..(2,3) in the update's H_B as well
+        env["SHIFTK_SPLIT_LO"] = "1"
+    _subprocess(SPLIT_FORCED, env)
 
 
 def test_tile_pairs_window_and_determinism():
