@@ -28,7 +28,10 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
     if (!spmv_enter(a, agent, buf, sc, kp)) return;
     constexpr int TS = 1 << T;
     constexpr int PER = TS / kThreads;
-    constexpr int NB = 3;
+#ifndef TILED_SPLIT_NB
+#define TILED_SPLIT_NB 3
+#endif
+    constexpr int NB = SPLIT ? TILED_SPLIT_NB : 3;   // partner tiles per round
     static_assert(PER * kThreads == TS, "tile must be a multiple of the CTA size");
     const cplx *__restrict__ r = pick3(a.r, buf);
     const cplx *__restrict__ t = pick3(a.t, buf);
