@@ -64,10 +64,18 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def bytes_per_row(problem, kernel: str) -> float:
-    """Algorithmic bytes per row of one launch."""
+def bytes_per_row(problem, kernel: str, plan=None) -> float:
+    """Algorithmic bytes per row of one launch.
+
+    With the bond split's fused r_{n-1} term (plan["split_fuse"]) the SpMV also
+    reads r_{n-1} (+16) and the update no longer does (-16): the iteration's total is unchanged."""
     nseq = 2 if problem.method == "bicg" else 1
+    shift = 16.0 if plan and plan.get("split_fuse") else 0.0
     if kernel == "spmv":
+        return bytes_per_row(problem, "spmv_") + shift
+    if kernel == "update":
+        return bytes_per_row(problem, "update_") - shift
+    if kernel == "spmv_":
         if problem.op["kind"] in ("heisenberg", "heisenberg_sz"):   # generated on the fly
             bh = 0.0
         else:
@@ -75,7 +83,7 @@ def bytes_per_row(problem, kernel: str) -> float:
             vb = 8 if problem.op["kind"] == "csr_real" else 16
             bh = nnz_row * (vb + 4) + 8
         return bh + 32.0 * nseq
-    if kernel == "update":
+    if kernel == "update_":
         b = 64.0 * nseq + 16.0 * problem.n_left
         if problem.full_x:
             b += 64.0 * problem.n_shift   # all shifts active during the timed window
@@ -474,7 +482,8 @@ def main():
     kernels = {"spmv": prof["ms_spmv"], "update": prof["ms_update"]}
     dom = max(kernels, key=kernels.get)
     per_launch_ms = kernels[dom] / max(prof["iterations"], 1)
-    alg_bytes = bytes_per_row(problem, dom) * problem.M / world   # this rank's rows
+    plan = solver.info()
+    alg_bytes = bytes_per_row(problem, dom, plan) * problem.M / world   # this rank's rows
     achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -500,7 +509,7 @@ def main():
         "active_shift_iterations_per_s": active_its / (total_ms * 1e-3),
         "gpu_launches": launches,
         "passes_ms": passes,
-        "plan": solver.info(),
+        "plan": plan,
         "solver_state": {"iterations": coeffs["iterations"], "n_active": coeffs["n_active"],
                          "switches": coeffs["switches"]},
     }

@@ -273,13 +273,18 @@ int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
 /* The execution plan sk_init chose for a context (diagnostics; bench.py reports it).
    split_ahi > 0: the Heisenberg bond split — the SpMV applies the diagonal and
    the bonds (i, i+1), i < split_ahi; the update kernel applies the bonds i >= split_ahi and the
-   periodic bond in its B-tile row order; 0: one kernel applies the whole operator. */
+   periodic bond in its B-tile row order; 0: one kernel applies the whole operator.
+   split_fuse: with the split, the SpMV also folds the r_{n-1} term of EQ-CG-RN-3REC into
+   its output, u = H_A r_n - (gamma sr_prev / sr_cur) r_{n-1}, so the update reads u and r_n only.
+   left_real: with the split and Im a = 0, the update reads Re a (8 B/row, its own row order). */
 typedef struct {
     int32_t split_ahi;       /* see above                                                      */
     int32_t spmv_ctas;       /* worker CTAs (= w partials) of the SpMV                         */
     int32_t update_ctas;     /* streaming CTAs of the update kernel                            */
     int32_t shift_agents;    /* shift-agent CTAs of the update kernel                          */
     int64_t arena_bytes;     /* device bytes the context owns                                  */
+    int32_t split_fuse;      /* see above                                                      */
+    int32_t left_real;       /* see above                                                      */
 } sk_info;
 int sk_get_info(sk_ctx *ctx, sk_info *out);
 

@@ -407,6 +407,8 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     if (kp.split_ahi) {
         kp.nblk_upd = sk::split_blocks();
         kp.split_lo = sk::split_lo_bonds();
+        // the fused r_{n-1} term lives in the tiled H_A kernel only
+        kp.split_fuse = sk::split_fuse_enabled() && !sk::heis_stream(H->L, M, kp.bicg, true);
     }
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
@@ -469,6 +471,10 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&kp.pibuf, sizeof(cplx) * 3 * c->nz);
         add(&kp.pi_frozen, sizeof(cplx) * c->nz);
         add(&kp.ticket, sizeof(uint32_t));
+        if (kp.split_ahi) {
+            add(&kp.kflag, 2 * sizeof(uint32_t));   // [0] SpMV kappa flag, [1] "Im a != 0 somewhere"
+            if (sk::split_left_real_enabled()) add(&kp.left_re, sizeof(double) * (size_t)M);
+        }
         add(&kp.work, 2 * sizeof(unsigned long long));
         add(&kp.amin_part, sizeof(AminPart) * 8);
         add(&kp.active, c->nz);
@@ -554,6 +560,14 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     if (sk::launch_init(kp, c->b, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init kernel"));
     if (kp.split_ahi && sk::launch_split_init(kp, c->stream) != cudaSuccess)
         return bail(fail(SK_ECUDA, "split init kernel"));
+    if (kp.split_ahi && kp.left_re) {   // a real left vector (Im a = 0): 8 B/row in B-tile order
+        uint32_t any_imag = 1;
+        if (sk::launch_split_left(kp, const_cast<double *>(kp.left_re), kp.kflag + 1, c->stream) != cudaSuccess ||
+            cudaMemcpyAsync(&any_imag, kp.kflag + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream) ||
+            cudaStreamSynchronize(c->stream))
+            return bail(fail(SK_ECUDA, "split left kernel"));
+        kp.left_real = any_imag ? 0 : 1;
+    }
     if (world > 1) {   // the global rho_0, ||b||, P b need the other ranks: finished at connect
         if (sk::launch_reduce_local(kp, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init reduce"));
         if (group) group->members[rank] = c;
@@ -674,6 +688,12 @@ int sk_restore(sk_ctx *c, const void *buf, size_t bytes) {
     if (c->world > 1) {
         CK(cudaMemcpyAsync((void *)c->kp.shard_r, keep_r.data(), tab, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync((void *)c->kp.shard_t, keep_t.data(), tab, cudaMemcpyHostToDevice, c->stream));
+    }
+    if (c->kp.split_ahi && c->kp.left_re) {   // the restored arena's left vector decides (kflag[1])
+        uint32_t any_imag = 1;
+        CK(cudaMemcpyAsync(&any_imag, c->kp.kflag + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->kp.left_real = any_imag ? 0 : 1;
     }
     CK(cudaStreamSynchronize(c->stream));
     c->pending_host = false;   // the checkpoint was taken after a finish
@@ -1078,6 +1098,8 @@ int sk_get_info(sk_ctx *c, sk_info *o) {
     o->update_ctas = c->kp.nblk_upd;
     o->shift_agents = c->kp.n_agents;
     o->arena_bytes = (int64_t)c->arena_bytes;
+    o->split_fuse = c->kp.split_fuse;
+    o->left_real = c->kp.left_real;
     return SK_OK;
 }
 

@@ -162,6 +162,15 @@ struct KParams {
     int32_t split_lo;            // bonds (i, i+1), i < split_lo, are in H_B too (B-tile piece bits)
     int64_t wsplit_off;
     double J;                    // exchange coupling of the Heisenberg operator (H_B amplitudes)
+    // fused r_{n-1} term (§5.9): the H_A SpMV writes u = H_A r_n - kappa r_{n-1} with
+    // kappa = gamma sr_prev / sr_cur (= -a_prev / a_q: known once the finish has fixed rho_n,
+    // before w_n), so the update reads u instead of q and r_{n-1} (80 -> 64 B/row there, 32 -> 48
+    // in the SpMV, which has DRAM headroom).  kflag: set by the SpMV's CTA 0 once the state is
+    // final (after its finish), awaited by the worker CTAs, cleared by the update kernel.
+    int32_t split_fuse;
+    int32_t left_real;           // kp.left_re holds Re a (Im a = 0) in B-tile order, 8 B/row
+    uint32_t *kflag;
+    const double *left_re;
     // per-shift arrays [nz]
     const cplx *z;
     cplx *pibuf;         // [3][nz] rotating pi_n^k

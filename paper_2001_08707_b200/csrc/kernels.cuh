@@ -117,6 +117,9 @@ int split_blocks();
 int split_lo_bonds();   // in-piece bonds (0,1).. moved from H_A to H_B (0: none)
 cudaError_t launch_update_split(const KParams &kp, const cplx *q, cudaStream_t s);
 cudaError_t launch_split_init(const KParams &kp, cudaStream_t s);
+int split_fuse_enabled();        // SHIFTK_SPLIT_FUSE (default 1): the H_A SpMV folds -kappa r_{n-1} into q
+int split_left_real_enabled();   // SHIFTK_LEFT_REAL (default 1): a real left vector is kept as Re a in B-tile order
+cudaError_t launch_split_left(const KParams &kp, double *out, uint32_t *any_imag, cudaStream_t s);
 
 // Single-CTA steps outside the iteration: INIT (after launch_init) and FINISH (residuals,
 // retirement, switch of a pending iteration).

@@ -17,8 +17,37 @@ namespace sk {
 // SPLIT (one GPU, COCG, N_left = 1): only H_A — the diagonal and the bonds
 // (i, i+1), i < kp.split_ahi; the periodic bond and the bonds i >= split_ahi are applied by the
 // update kernel (update_split.cu).
+// TILED_FUSE_EARLY = 1: the fused r_{n-1} term enters q in round 1 (r_{n-1} loaded beside the own
+// tile; w corrected by kappa <r_n, r_{n-1}> at the end); 0: added last, after the in-tile bonds.
+#ifndef TILED_FUSE_EARLY
+#define TILED_FUSE_EARLY 1
+#endif
+#ifndef TILED_SPLIT_MINB
+#define TILED_SPLIT_MINB 4   // resident CTAs per SM the SPLIT kernel is compiled for (register cap)
+#endif
+
+// Worker CTAs of the fused SPLIT kernel, once per launch (CTA-uniform; ends with a barrier): wait
+// until CTA 0 has published the final state (kp.kflag), then -kappa = -gamma sr_prev / sr_cur
+// (steps.cuh seed_compute: a_prev / a_q) into *out.  Returns 1 when kappa == 0 (first iteration:
+// r_{n-1} does not exist yet), else 2.
+static __device__ __noinline__ int wait_kappa(const uint32_t *kflag, const DevState *st, cplx *out) {
+    if (threadIdx.x == 0) {
+        unsigned f;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(kflag) : "memory");
+            if (!f) __nanosleep(100);
+        } while (!f);
+        const cplx g = __ldcg(&st->gamma_nx), sp = __ldcg(&st->sr_prev), sc_ = __ldcg(&st->sr_cur);
+        cplx kap = mk(0.0, 0.0);
+        if (g.x != 0.0 || g.y != 0.0) kap = xdiv(cmul(g, sp), sc_);
+        *out = mk(-kap.x, -kap.y);
+    }
+    __syncthreads();
+    return (out->x == 0.0 && out->y == 0.0) ? 1 : 2;
+}
+
 template <int L, int T, int NRHS, bool MULTI, bool SPLIT = false>
-__global__ void __launch_bounds__(kThreads, NRHS == 1 ? 4 : 2)
+__global__ void __launch_bounds__(kThreads, NRHS == 1 ? (SPLIT ? TILED_SPLIT_MINB : 4) : 2)
 heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
     extern __shared__ cplx tile[];   // [NRHS][2^T]
     __shared__ StepScratch sc;
@@ -39,15 +68,36 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
     // through peer memory; every partner tile below is resolved once per tile (its shard is
     // uniform over the tile).
     const RViewT<MULTI> rv = rview<MULTI>(r, kp.shard_r, buf, kp), tv = rview<MULTI>(t, kp.shard_t, buf, kp);
+    // SPLIT with the fused r_{n-1} term (kp.split_fuse, §5.9): q <- H_A r_n - kappa r_{n-1}.  CTA 0
+    // publishes that the state is final (its finish fixed gamma and the lazy scales); a worker
+    // needs kappa only at the end of its first tile.
+    const bool fuse = SPLIT && kp.split_fuse != 0;
+    __shared__ cplx s_nkap;   // -kappa
+    int kstate = 0;           // 0: not read yet, 1: kappa == 0 (first iteration), 2: kappa != 0
+    if (SPLIT && fuse && agent) {
+        __threadfence();
+        __syncthreads();   // the finish's state_store is complete
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(kp.kflag), "r"(1u) : "memory");
+        }
+    }
     const double qJ = 0.25 * J, hJ = 0.5 * J;
     const int64_t ntiles = a.M >> T;
     const int tid = threadIdx.x;
     const int off = a.st ? 1 : 0;
+    // early variant: kappa before the first tile (the workers idle for the ~15 us of CTA 0's
+    // finish, once per launch; a wait inside the loop costs registers across the call)
+    if (SPLIT && TILED_FUSE_EARLY && fuse && !agent) kstate = wait_kappa(kp.kflag, a.st, &s_nkap);
     cplx w = mk(0.0, 0.0);
     for (int64_t ti = (int64_t)blockIdx.x - off; !agent && ti < ntiles; ti += gridDim.x - off) {
         const int64_t lbase = ti << T;                  // local row of the tile
         const U base = (U)((MULTI ? rv.row0 : 0) + lbase);   // global basis state of the tile
         __syncthreads();   // previous tile's shared-memory reads are done
+        // (late variant) r_{n-1} of the tile's rows is needed last: one bulk L2 prefetch now (no
+        // register or L1 cost), the loads themselves after the in-tile bonds
+        if (SPLIT && fuse && !TILED_FUSE_EARLY && kstate != 1 && tid == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pick3(a.r, buf + 2) + lbase), "r"((unsigned)(sizeof(cplx) << T)) : "memory");
         cplx q[PER], qt[NRHS == 2 ? PER : 1];
         {
             cplx v0[PER], v1[PER], v2[PER], t0[NRHS == 2 ? PER : 1], t1[NRHS == 2 ? PER : 1],
@@ -68,9 +118,14 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 v1[k] = on1 ? p1[l1] : mk(0.0, 0.0);
                 if (NRHS == 2) t1[k] = on1 ? p1t[l1] : mk(0.0, 0.0);
                 const bool on2 = !SPLIT && ((U)(ls & 1) ^ hb) != 0;      // bond (L-1, 0)
-                v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
+                if (SPLIT && TILED_FUSE_EARLY)   // no periodic bond in H_A: v2 carries r_{n-1} instead
+                    v2[k] = (fuse && kstate != 1) ? ldg_cs(pick3(a.r, buf + 2) + lbase + ls) : mk(0.0, 0.0);
+                else
+                    v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
                 if (NRHS == 2) t2[k] = on2 ? p2t[ls ^ 1] : mk(0.0, 0.0);
             }
+            cplx nkap = mk(0.0, 0.0), wr = mk(0.0, 0.0);
+            if (SPLIT && TILED_FUSE_EARLY && fuse) nkap = s_nkap;
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const int ls = tid + k * kThreads;
@@ -79,12 +134,31 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 const int na = (L <= 31) ? __popc((unsigned)x) : __popcll((unsigned long long)x);
                 const double d = qJ * (double)(L - 2 * na);
                 tile[ls] = v0[k];
-                q[k].x = fma(hJ, v1[k].x + v2[k].x, d * v0[k].x);
-                q[k].y = fma(hJ, v1[k].y + v2[k].y, d * v0[k].y);
+                if (SPLIT && TILED_FUSE_EARLY) {   // q = H_A r - kappa r_{n-1}; wr = <r_n, r_{n-1}> of the tile
+                    q[k].x = fma(hJ, v1[k].x, d * v0[k].x);
+                    q[k].y = fma(hJ, v1[k].y, d * v0[k].y);
+                    q[k] = cfma(nkap, v2[k], q[k]);
+                    wr = cfma(v0[k], v2[k], wr);   // <r_n, r_{n-1}> of the thread's rows
+                } else {
+                    q[k].x = fma(hJ, v1[k].x + v2[k].x, d * v0[k].x);
+                    q[k].y = fma(hJ, v1[k].y + v2[k].y, d * v0[k].y);
+                }
                 if (NRHS == 2) {
                     tile[TS + ls] = t0[k];
                     qt[k].x = fma(hJ, t1[k].x + t2[k].x, d * t0[k].x);
                     qt[k].y = fma(hJ, t1[k].y + t2[k].y, d * t0[k].y);
+                }
+            }
+            // w is taken from q below, with the fused term inside: <r, H_A r> = <r, u> + kappa <r_n, r_{n-1}>
+            if (SPLIT && TILED_FUSE_EARLY) w = cfma(mk(-nkap.x, -nkap.y), wr, w);
+            // bond (T-2, T-1) = local bits (8, 9) = the thread's own k: states k = 1, 2 are each
+            // other's partner, still in registers here
+            if (PER == 4) {
+                q[1].x = fma(hJ, v0[2].x, q[1].x); q[1].y = fma(hJ, v0[2].y, q[1].y);
+                q[2].x = fma(hJ, v0[1].x, q[2].x); q[2].y = fma(hJ, v0[1].y, q[2].y);
+                if (NRHS == 2) {
+                    qt[1].x = fma(hJ, t0[2].x, qt[1].x); qt[1].y = fma(hJ, t0[2].y, qt[1].y);
+                    qt[2].x = fma(hJ, t0[1].x, qt[2].x); qt[2].y = fma(hJ, t0[1].y, qt[2].y);
                 }
             }
         }
@@ -158,8 +232,8 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
         // Bonds (i, i+1), i < T-1, inside the tile.  The tile's low bits of state ls = tid + 256 k
         // are tid (bits 0..7) and k (bits 8, 9), so: bonds i <= 6 are decided by tid alone (one
         // test per thread, the four states' partners at tid ^ (3 << i) + 256 k: constant
-        // offsets); bond 7 by tid bit 7 and k bit 0 (partner k ^ 1); bond 8 by k alone — a
-        // compile-time choice between the thread's own states.
+        // offsets); bond 7 by tid bit 7 and k bit 0 (partner k ^ 1); bond 8 by k alone — between
+        // the thread's own states, applied in round 1 while they were in registers.
         static_assert(T == 10 && kThreads == 256 && PER == 4, "bit split assumes 1024-state tiles");
         {
             const unsigned xt = (unsigned)(tid ^ (tid >> 1));
@@ -194,28 +268,32 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                         qt[k].y = fma(hJ, vt.y, qt[k].y);
                     }
                 }
-                if ((k ^ (k >> 1)) & 1) {   // bond (8, 9): k = 1, 2, partner k ^ 3
-                    const cplx v = tile[tid + (k ^ 3) * kThreads];
-                    q[k].x = fma(hJ, v.x, q[k].x);
-                    q[k].y = fma(hJ, v.y, q[k].y);
-                    if (NRHS == 2) {
-                        const cplx vt = tile[TS + tid + (k ^ 3) * kThreads];
-                        qt[k].x = fma(hJ, vt.x, qt[k].x);
-                        qt[k].y = fma(hJ, vt.y, qt[k].y);
-                    }
-                }
+                // (bond (8, 9) was applied from registers in round 1)
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {   // w = <r~|r, H r> of the tile (before the fused term)
+            const int ls = tid + k * kThreads;
+            if (NRHS == 2) w = cfma_conj(tile[TS + ls], q[k], w);
+            else w = cfma(tile[ls], q[k], w);
+        }
+        if (SPLIT && fuse && !TILED_FUSE_EARLY) {
+            if (kstate == 0) kstate = wait_kappa(kp.kflag, a.st, &s_nkap);   // once per CTA (uniform)
+            if (kstate == 2) {
+                const cplx *__restrict__ rpv = pick3(a.r, buf + 2) + lbase + tid;   // r_{n-1} (stored form)
+                cplx rp[PER];
+#pragma unroll
+                for (int k = 0; k < PER; ++k) rp[k] = ldg_cs(rpv + k * kThreads);
+                const cplx nkap = s_nkap;
+#pragma unroll
+                for (int k = 0; k < PER; ++k) q[k] = cfma(nkap, rp[k], q[k]);
             }
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int ls = tid + k * kThreads;
             a.q[lbase + ls] = q[k];
-            if (NRHS == 2) {
-                a.qt[lbase + ls] = qt[k];
-                w = cfma_conj(tile[TS + ls], q[k], w);
-            } else {
-                w = cfma(tile[ls], q[k], w);
-            }
+            if (NRHS == 2) a.qt[lbase + ls] = qt[k];
         }
     }
     spmv_exit(a, kp, agent, w, sc);

@@ -93,7 +93,10 @@ struct BondView {
     }
 };
 
-template <int HB, int TB, int NT>
+// FUSE: q holds u = H_A r_n - kappa r_{n-1} (the SpMV's fused r_{n-1} term, kp.split_fuse), so
+// r_{n+1} = a_cur r_n + a_q (u + H_B r_n) and r_{n-1} is not read.  LRE: the left vector is real
+// (Im a = 0 at initialisation) and kp.left_re holds it in B-tile order (8 B/row, linear).
+template <int HB, int TB, int NT, bool FUSE, bool LRE>
 __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const cplx *__restrict__ q) {
     constexpr int TS = 1 << TB, PER = TS / NT, PB = TB - HB;
     constexpr int NB = NT == 256 ? 8 : NT == 512 ? 9 : 10;
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
     __shared__ cplx scratch[4 * (NT / 32)];
     pdl_wait();
     DevState *st = kp.st;
+    if (FUSE && blockIdx.x == 0 && threadIdx.x == 0) *kp.kflag = 0u;   // the SpMV grid is complete
     if (st->status != ST_ITERATING) return;
     const int wb = blockIdx.x - kp.n_agents, nwb = gridDim.x - kp.n_agents;
     const int ahi = kp.split_ahi;
@@ -157,19 +161,22 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
     const cplx a_cur = us.o.a_cur, a_q = us.o.a_q, a_prev = us.o.a_prev;
     const double hJ = 0.5 * kp.J;
     const cplx *__restrict__ left = kp.left;
+    const double *__restrict__ left_re = kp.left_re;
     const bool lo = kp.split_lo != 0;   // the piece bonds (0,1)..(PB-2,PB-1) are in H_B
     cplx rho = mk(0.0, 0.0), nu = mk(0.0, 0.0), g = mk(0.0, 0.0), wbp = mk(0.0, 0.0);
     for (int64_t t = wb; t < ntiles; t += nwb) {
         // every row-stream load of the tile is issued before waiting for its staged r_n (they do
         // not depend on it): 3 PER loads in flight per thread across the wait and the barrier
         const int64_t rt = row0 + (t << PB);
-        cplx qa[PER], rp[PER], lv[PER];
+        cplx qa[PER], rp[FUSE ? 1 : PER], lv[LRE ? 1 : PER];
+        double lr[LRE ? PER : 1];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int64_t s = rt + k * kstep;
             qa[k] = ldg_cs(q + s);
-            rp[k] = ldg_cs(rp_ + s);
-            lv[k] = ldg_cs(left + s);
+            if (!FUSE) rp[FUSE ? 0 : k] = ldg_cs(rp_ + s);
+            if (LRE) lr[LRE ? k : 0] = __ldcs(left_re + (t << TB) + (tid | (k << NB)));
+            else lv[LRE ? 0 : k] = ldg_cs(left + s);
         }
         cp_async_wait<0>();   // this tile's r_n has landed (staged during the previous w_B pass)
         __syncthreads();      // ... for every thread; and W of the previous tile is consumed
@@ -188,12 +195,13 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
             const cplx qf = mk(fma(hJ, h.x, qa[k].x), fma(hJ, h.y, qa[k].y));   // (H r_n)_s
             cplx rn = cmul(a_cur, S[e]);
             rn = cfma(a_q, qf, rn);
-            rn = cfma(a_prev, rp[k], rn);
+            if (!FUSE) rn = cfma(a_prev, rp[FUSE ? 0 : k], rn);
             rn_[rt + k * kstep] = rn;
             W[e] = rn;
             rho = cfma(rn, rn, rho);
             nu.x = fma(rn.x, rn.x, fma(rn.y, rn.y, nu.x));
-            g = cfma_conj(lv[k], rn, g);
+            if (LRE) g = mk(fma(lr[LRE ? k : 0], rn.x, g.x), fma(lr[LRE ? k : 0], rn.y, g.y));
+            else g = cfma_conj(lv[LRE ? 0 : k], rn, g);
         }
         __syncthreads();   // r_{n+1} of the tile complete in W; r_n no longer read
         if (t + nwb < ntiles) stage(t + nwb);   // in flight during the w_B pass
@@ -265,6 +273,20 @@ __global__ void __launch_bounds__(NT, 1) split_wb_kernel(KParams kp, const cplx 
     if (threadIdx.x == 0) out[blockIdx.x] = v[0];
 }
 
+// Re a in B-tile order (left_re[(t << TB) | e] = Re a[split_row(t, e)]) and a flag word that is
+// nonzero when some Im a != 0 (then the complex left vector is read as before).
+template <int HB, int TB>
+__global__ void split_left_kernel(KParams kp, double *out, uint32_t *any_imag) {
+    const int ahi = kp.split_ahi;
+    bool im = false;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < kp.M; j += (int64_t)gridDim.x * blockDim.x) {
+        const cplx v = kp.left[split_row<HB, TB>(j >> TB, (int)(j & ((1 << TB) - 1)), ahi)];
+        out[j] = v.x;
+        im |= v.y != 0.0;
+    }
+    if (__syncthreads_or(im) && threadIdx.x == 0) atomicOr(any_imag, 1u);
+}
+
 // ---- host side --------------------------------------------------------------------------------
 int split_ahi_for(int L, int64_t M, int world, int bicg, int full, int nl, int kind_heisenberg) {
     static int en = -2;
@@ -297,11 +319,19 @@ int split_blocks() { return sm_count(); }   // one CTA per SM (128 KB of shared 
 static size_t split_smem_update() { return 2 * (sizeof(cplx) << kSplitTB); }
 static size_t split_smem_init() { return sizeof(cplx) << kSplitTB; }
 
+template <bool FUSE, bool LRE>
+static cudaError_t split_attr() {
+    return cudaFuncSetAttribute(update_split_kernel<kSplitHB, kSplitTB, kSplitNT, FUSE, LRE>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem_update());
+}
+
 static cudaError_t split_setup() {
     static PerDevice once;
     return once_per_device(once, [] {
-        cudaError_t e = cudaFuncSetAttribute(update_split_kernel<kSplitHB, kSplitTB, kSplitNT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem_update());
+        cudaError_t e = split_attr<false, false>();
+        if (e == cudaSuccess) e = split_attr<false, true>();
+        if (e == cudaSuccess) e = split_attr<true, false>();
+        if (e == cudaSuccess) e = split_attr<true, true>();
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(split_wb_kernel<kSplitHB, kSplitTB, kSplitNT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem_init());
@@ -309,11 +339,45 @@ static cudaError_t split_setup() {
     });
 }
 
+template <bool FUSE, bool LRE>
+static cudaError_t launch_update_split_t(const KParams &kp, const cplx *q, cudaStream_t s) {
+    return launch_k(update_split_kernel<kSplitHB, kSplitTB, kSplitNT, FUSE, LRE>, kp.nblk_upd + kp.n_agents,
+                    kSplitNT, split_smem_update(), s, true, kp, q);
+}
+
 cudaError_t launch_update_split(const KParams &kp, const cplx *q, cudaStream_t s) {
     const cudaError_t e = split_setup();
     if (e != cudaSuccess) return e;
-    return launch_k(update_split_kernel<kSplitHB, kSplitTB, kSplitNT>, kp.nblk_upd + kp.n_agents, kSplitNT,
-                    split_smem_update(), s, true, kp, q);
+    if (kp.split_fuse)
+        return kp.left_real ? launch_update_split_t<true, true>(kp, q, s) : launch_update_split_t<true, false>(kp, q, s);
+    return kp.left_real ? launch_update_split_t<false, true>(kp, q, s) : launch_update_split_t<false, false>(kp, q, s);
+}
+
+// SHIFTK_SPLIT_FUSE=0: the SpMV writes plain q = H_A r and the update reads r_{n-1} itself.
+// (The streaming H_A kernel never fuses.)
+int split_fuse_enabled() {
+    static int en = -1;
+    if (en < 0) {
+        const char *e = getenv("SHIFTK_SPLIT_FUSE");
+        en = (e && e[0] == '0') ? 0 : 1;
+    }
+    return en;
+}
+
+// SHIFTK_LEFT_REAL=0: never use the compressed real left vector.
+int split_left_real_enabled() {
+    static int en = -1;
+    if (en < 0) {
+        const char *e = getenv("SHIFTK_LEFT_REAL");
+        en = (e && e[0] == '0') ? 0 : 1;
+    }
+    return en;
+}
+
+// out = Re(kp.left) in B-tile order; *any_imag |= 1 when some Im != 0 (zeroed by the caller)
+cudaError_t launch_split_left(const KParams &kp, double *out, uint32_t *any_imag, cudaStream_t s) {
+    split_left_kernel<kSplitHB, kSplitTB><<<8 * sm_count(), 256, 0, s>>>(kp, out, any_imag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_split_init(const KParams &kp, cudaStream_t s) {
