@@ -17,10 +17,10 @@ namespace sk {
 // SPLIT (one GPU, COCG, N_left = 1): only H_A — the diagonal and the bonds
 // (i, i+1), i < kp.split_ahi; the periodic bond and the bonds i >= split_ahi are applied by the
 // update kernel (update_split.cu).
-// TILED_FUSE_EARLY = 1: the fused r_{n-1} term enters q in round 1 (r_{n-1} loaded beside the own
-// tile; w corrected by kappa <r_n, r_{n-1}> at the end); 0: added last, after the in-tile bonds.
-#ifndef TILED_FUSE_EARLY
-#define TILED_FUSE_EARLY 1
+// TILED_SPLIT_QCS = 1: the SPLIT kernel's output is stored evict-first (st.global.cs): at the
+// chain lengths of the split the update reads it from DRAM anyway, and L2 keeps more of r.
+#ifndef TILED_SPLIT_QCS
+#define TILED_SPLIT_QCS 1
 #endif
 #ifndef TILED_SPLIT_MINB
 #define TILED_SPLIT_MINB 4   // resident CTAs per SM the SPLIT kernel is compiled for (register cap)
@@ -86,17 +86,15 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
     const int64_t ntiles = a.M >> T;
     const int tid = threadIdx.x;
     const int off = a.st ? 1 : 0;
-    // early variant: kappa before the first tile (the workers idle for the ~15 us of CTA 0's
-    // finish, once per launch; a wait inside the loop costs registers across the call)
-    if (SPLIT && TILED_FUSE_EARLY && fuse && !agent) kstate = wait_kappa(kp.kflag, a.st, &s_nkap);
     cplx w = mk(0.0, 0.0);
     for (int64_t ti = (int64_t)blockIdx.x - off; !agent && ti < ntiles; ti += gridDim.x - off) {
         const int64_t lbase = ti << T;                  // local row of the tile
         const U base = (U)((MULTI ? rv.row0 : 0) + lbase);   // global basis state of the tile
         __syncthreads();   // previous tile's shared-memory reads are done
-        // (late variant) r_{n-1} of the tile's rows is needed last: one bulk L2 prefetch now (no
-        // register or L1 cost), the loads themselves after the in-tile bonds
-        if (SPLIT && fuse && !TILED_FUSE_EARLY && kstate != 1 && tid == 0)
+        // r_{n-1} of the tile's rows is needed last: one bulk L2 prefetch now (no register or L1
+        // cost; a normal-priority fill — evict-first loads that MISS L2 wrecked the partner tiles'
+        // hit rate, 52% -> 22%), the loads themselves after the in-tile bonds
+        if (SPLIT && fuse && kstate != 1 && tid == 0)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pick3(a.r, buf + 2) + lbase), "r"((unsigned)(sizeof(cplx) << T)) : "memory");
         cplx q[PER], qt[NRHS == 2 ? PER : 1];
         {
@@ -118,14 +116,9 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 v1[k] = on1 ? p1[l1] : mk(0.0, 0.0);
                 if (NRHS == 2) t1[k] = on1 ? p1t[l1] : mk(0.0, 0.0);
                 const bool on2 = !SPLIT && ((U)(ls & 1) ^ hb) != 0;      // bond (L-1, 0)
-                if (SPLIT && TILED_FUSE_EARLY)   // no periodic bond in H_A: v2 carries r_{n-1} instead
-                    v2[k] = (fuse && kstate != 1) ? ldg_cs(pick3(a.r, buf + 2) + lbase + ls) : mk(0.0, 0.0);
-                else
-                    v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
+                v2[k] = on2 ? p2[ls ^ 1] : mk(0.0, 0.0);
                 if (NRHS == 2) t2[k] = on2 ? p2t[ls ^ 1] : mk(0.0, 0.0);
             }
-            cplx nkap = mk(0.0, 0.0), wr = mk(0.0, 0.0);
-            if (SPLIT && TILED_FUSE_EARLY && fuse) nkap = s_nkap;
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const int ls = tid + k * kThreads;
@@ -134,23 +127,14 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 const int na = (L <= 31) ? __popc((unsigned)x) : __popcll((unsigned long long)x);
                 const double d = qJ * (double)(L - 2 * na);
                 tile[ls] = v0[k];
-                if (SPLIT && TILED_FUSE_EARLY) {   // q = H_A r - kappa r_{n-1}; wr = <r_n, r_{n-1}> of the tile
-                    q[k].x = fma(hJ, v1[k].x, d * v0[k].x);
-                    q[k].y = fma(hJ, v1[k].y, d * v0[k].y);
-                    q[k] = cfma(nkap, v2[k], q[k]);
-                    wr = cfma(v0[k], v2[k], wr);   // <r_n, r_{n-1}> of the thread's rows
-                } else {
-                    q[k].x = fma(hJ, v1[k].x + v2[k].x, d * v0[k].x);
-                    q[k].y = fma(hJ, v1[k].y + v2[k].y, d * v0[k].y);
-                }
+                q[k].x = fma(hJ, v1[k].x + v2[k].x, d * v0[k].x);
+                q[k].y = fma(hJ, v1[k].y + v2[k].y, d * v0[k].y);
                 if (NRHS == 2) {
                     tile[TS + ls] = t0[k];
                     qt[k].x = fma(hJ, t1[k].x + t2[k].x, d * t0[k].x);
                     qt[k].y = fma(hJ, t1[k].y + t2[k].y, d * t0[k].y);
                 }
             }
-            // w is taken from q below, with the fused term inside: <r, H_A r> = <r, u> + kappa <r_n, r_{n-1}>
-            if (SPLIT && TILED_FUSE_EARLY) w = cfma(mk(-nkap.x, -nkap.y), wr, w);
             // bond (T-2, T-1) = local bits (8, 9) = the thread's own k: states k = 1, 2 are each
             // other's partner, still in registers here
             if (PER == 4) {
@@ -277,7 +261,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
             if (NRHS == 2) w = cfma_conj(tile[TS + ls], q[k], w);
             else w = cfma(tile[ls], q[k], w);
         }
-        if (SPLIT && fuse && !TILED_FUSE_EARLY) {
+        if (SPLIT && fuse) {
             if (kstate == 0) kstate = wait_kappa(kp.kflag, a.st, &s_nkap);   // once per CTA (uniform)
             if (kstate == 2) {
                 const cplx *__restrict__ rpv = pick3(a.r, buf + 2) + lbase + tid;   // r_{n-1} (stored form)
@@ -292,7 +276,8 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int ls = tid + k * kThreads;
-            a.q[lbase + ls] = q[k];
+            if (SPLIT && TILED_SPLIT_QCS) stg_cs(a.q + lbase + ls, q[k]);
+            else a.q[lbase + ls] = q[k];
             if (NRHS == 2) a.qt[lbase + ls] = qt[k];
         }
     }

@@ -376,6 +376,49 @@ def test_bond_split_forced_at_small_l(a_kernel):
     _subprocess(SPLIT_FORCED, env)
 
 
+SPLIT_MODES = """
+import dataclasses, os
+import numpy as np, oracle, synth
+from paper_2001_08707_b200.device import make_solver, to_device
+from test_gpu_parity import run_window
+want_fuse, want_real = int(os.environ["WANT_FUSE"]), int(os.environ["WANT_REAL"])
+p = synth.make_problem("c2", L=20, nz=64)
+if os.environ.get("COMPLEX_LEFT"):   # one explicit complex left vector (a != b): Im a != 0
+    rng = np.random.Generator(np.random.PCG64(11))
+    a = rng.standard_normal(p.M) + 1j * rng.standard_normal(p.M)
+    p = dataclasses.replace(p, left=(a / np.linalg.norm(a)).reshape(1, -1))
+g, o, wr, wy = run_window(p, 30)
+i = g.info()
+assert i["split_ahi"] == 12 and i["split_fuse"] == want_fuse and i["left_real"] == want_real, i
+h = make_solver(to_device(p))   # graph-captured == stepwise, bit for bit
+h.run(g.iterations, poll_every=g.iterations)
+assert np.array_equal(g.residuals(), h.residuals()) and np.array_equal(g.projections(), h.projections())
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("mode", ["plain", "fuse-only", "real-only", "complex-left"])
+def test_bond_split_fuse_and_real_left_switches(mode):
+    """The bond split's fused r_{n-1} term (u = H_A r_n - kappa r_{n-1} written by the SpMV) and
+    its real left vector in B-tile order switched off one at a time
+    (SHIFTK_SPLIT_FUSE=0 / SHIFTK_LEFT_REAL=0), and a complex left vector (the flag raised at
+    init sends the update back to the complex stream): each a 30-iteration oracle window at
+    L = 20 with the split forced; the default (both on) is test_bond_split_forced_at_small_l."""
+    env = {"SHIFTK_HEIS_SPLIT": "1", "SHIFTK_HEIS_STREAM": "0"}
+    fuse, real = 1, 1
+    if mode in ("plain", "real-only"):
+        env["SHIFTK_SPLIT_FUSE"] = "0"
+        fuse = 0
+    if mode in ("plain", "fuse-only"):
+        env["SHIFTK_LEFT_REAL"] = "0"
+        real = 0
+    if mode == "complex-left":
+        env["COMPLEX_LEFT"] = "1"
+        real = 0
+    env.update(WANT_FUSE=str(fuse), WANT_REAL=str(real))
+    _subprocess(SPLIT_MODES, env)
+
+
 def test_tile_pairs_window_and_determinism():
     """L=24 with the bond split off (SHIFTK_HEIS_SPLIT=0): the streaming SpMV works on tile pairs
     across the top spin bit (each the other's periodic partner); oracle window and bit-identical
