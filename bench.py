@@ -522,6 +522,10 @@ def main():
                                          "model": "element reads of other ranks' rows per iteration "
                                                   "(paper_2001_08707_b200/dist.py remote_rows_per_spmv)"}
 
+    # the timed solver's arena (C5: 94 GB) is released before the end-to-end leg builds its own
+    solver.finalize()
+    torch.cuda.empty_cache()
+
     # end-to-end through the public API with HOST buffers (pinned b in, results out)
     if not args.no_e2e:
         src_b = problem.b if sl is None else sl.b

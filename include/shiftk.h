@@ -276,7 +276,10 @@ int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
    periodic bond in its B-tile row order; 0: one kernel applies the whole operator.
    split_fuse: with the split, the SpMV also folds the r_{n-1} term of EQ-CG-RN-3REC into
    its output, u = H_A r_n - (gamma sr_prev / sr_cur) r_{n-1}, so the update reads u and r_n only.
-   left_real: with the split and Im a = 0, the update reads Re a (8 B/row, its own row order). */
+   left_real: with the split and Im a = 0, the update reads Re a (8 B/row, its own row order).
+   csr_col_blocks: chosen at sk_init for a CSR operator whose vector is well beyond L2 when the
+   rows are sorted by column, at most 255 entries long, and a quarter or more of the entries lie
+   at least half a block from the diagonal (SHIFTK_CSR_BLOCKED=0/1 disables / forces it). */
 typedef struct {
     int32_t split_ahi;       /* see above                                                      */
     int32_t spmv_ctas;       /* worker CTAs (= w partials) of the SpMV                         */
@@ -285,6 +288,8 @@ typedef struct {
     int64_t arena_bytes;     /* device bytes the context owns                                  */
     int32_t split_fuse;      /* see above                                                      */
     int32_t left_real;       /* see above                                                      */
+    int32_t csr_col_blocks;  /* >= 2: the CSR SpMV runs that many passes over column blocks of  */
+    int32_t csr_block_shift; /* 2^csr_block_shift rows (the gathered slice of r stays in L2); 0: one pass */
 } sk_info;
 int sk_get_info(sk_ctx *ctx, sk_info *out);
 

@@ -194,7 +194,7 @@ static int enqueue_phase_a(sk_ctx *c, const cplx *q_rc, const cplx *qt_rc, sk::S
         CK(sk::launch_csr(a, c->kp, c->op.row_ptr, c->op.col, c->op.val, c->op.kind == SK_OP_CSR_CPLX,
                           c->avg_nnz, c->stream));
     CK(prof_mark(c));
-    if (!c->capturing) c->launches += 1;
+    if (!c->capturing) c->launches += (!q_rc && c->kp.csr_nblk >= 2) ? c->kp.csr_nblk : 1;
     return SK_OK;
 }
 
@@ -410,6 +410,15 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         // the fused r_{n-1} term lives in the tiled H_A kernel only
         kp.split_fuse = sk::split_fuse_enabled() && !sk::heis_stream(H->L, M, kp.bicg, true);
     }
+    // column-blocked CSR passes (spmv.cu): a candidate when the vector is well beyond L2 (or when
+    // forced); the split kernel below decides from the rows themselves
+    int csr_cand_nblk = 0;
+    if ((H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) && world == 1 && sk::csr_blocked_env() != 0) {
+        const int bs = sk::csr_block_shift();
+        const int64_t nb = (M + (int64_t(1) << bs) - 1) >> bs;
+        const bool big = (size_t)M * sizeof(cplx) >= (size_t(96) << 20);
+        if (nb >= 2 && nb <= 16 && M < (int64_t(1) << 31) && (big || sk::csr_blocked_env() == 1)) csr_cand_nblk = (int)nb;
+    }
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
     kp.rank = rank;
@@ -421,6 +430,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
     // One device arena for everything the context owns (one cudaMalloc / cudaFree); every
     // array is padded to 256 B so bulk (TMA) copies of rounded sizes stay inside it.
     cplx *zdev = nullptr;
+    unsigned long long *csr_stats = nullptr;
     {
         struct Item { void **p; size_t bytes; };
         std::vector<Item> items;
@@ -471,6 +481,10 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         add(&kp.pibuf, sizeof(cplx) * 3 * c->nz);
         add(&kp.pi_frozen, sizeof(cplx) * c->nz);
         add(&kp.ticket, sizeof(uint32_t));
+        if (csr_cand_nblk) {
+            add(&kp.csr_split, (size_t)(csr_cand_nblk + 1) * (size_t)M);
+            add(&csr_stats, 2 * sizeof(unsigned long long));
+        }
         if (kp.split_ahi) {
             add(&kp.kflag, 2 * sizeof(uint32_t));   // [0] SpMV kappa flag, [1] "Im a != 0 somewhere"
             if (sk::split_left_real_enabled()) add(&kp.left_re, sizeof(double) * (size_t)M);
@@ -556,6 +570,21 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
             return bail(fail(SK_ECUDA, "init state"));
         // the pinned mirror is reused below; make sure the copy has consumed it
         if (cudaStreamSynchronize(c->stream)) return bail(fail(SK_ECUDA, "sync"));
+    }
+    if (csr_cand_nblk) {   // split points of the column blocks; blocking applies when the rows are
+                           // sorted, short, and enough gathers are far (or it is forced)
+        unsigned long long st2[2] = {1, 0};
+        const int bs = sk::csr_block_shift();
+        if (sk::launch_csr_split(M, H->row_ptr, H->col, csr_cand_nblk, bs, const_cast<uint8_t *>(kp.csr_split),
+                                 csr_stats, c->stream) != cudaSuccess ||
+            cudaMemcpyAsync(st2, csr_stats, sizeof(st2), cudaMemcpyDeviceToHost, c->stream) ||
+            cudaStreamSynchronize(c->stream))
+            return bail(fail(SK_ECUDA, "csr split kernel"));
+        const bool far = (double)st2[1] >= 0.25 * (double)H->nnz;
+        if (st2[0] == 0 && (far || sk::csr_blocked_env() == 1)) {
+            kp.csr_nblk = csr_cand_nblk;
+            kp.csr_bshift = bs;
+        }
     }
     if (sk::launch_init(kp, c->b, c->stream) != cudaSuccess) return bail(fail(SK_ECUDA, "init kernel"));
     if (kp.split_ahi && sk::launch_split_init(kp, c->stream) != cudaSuccess)
@@ -917,7 +946,8 @@ static int enqueue_iters(sk_ctx *c, int64_t iters, int chunk, bool single1 = fal
     if (iters >= chunk && chunk > 1) {
         if ((rc = capture_graph(c, chunk)) != SK_OK) return rc;
     }
-    const int kpi = c->world > 1 ? 3 : 2;   // kernels per iteration (+ the seed kernel)
+    // kernels per iteration (+ the seed kernel with several ranks; + the extra column-block passes)
+    const int kpi = (c->world > 1 ? 3 : 2) + (c->kp.csr_nblk >= 2 ? c->kp.csr_nblk - 1 : 0);
     while (iters >= chunk && chunk > 1) {
         CK(cudaGraphLaunch(c->graph, c->stream));
         c->launches += kpi * chunk;
@@ -1100,6 +1130,8 @@ int sk_get_info(sk_ctx *c, sk_info *o) {
     o->arena_bytes = (int64_t)c->arena_bytes;
     o->split_fuse = c->kp.split_fuse;
     o->left_real = c->kp.left_real;
+    o->csr_col_blocks = c->kp.csr_nblk;
+    o->csr_block_shift = c->kp.csr_nblk ? c->kp.csr_bshift : 0;
     return SK_OK;
 }
 

@@ -171,6 +171,11 @@ struct KParams {
     int32_t left_real;           // kp.left_re holds Re a (Im a = 0) in B-tile order, 8 B/row
     uint32_t *kflag;
     const double *left_re;
+    // column-blocked CSR SpMV (spmv.cu): csr_nblk >= 2 passes over column blocks
+    // of 2^csr_bshift rows, so the gathered slice of r stays in L2; csr_split[b * M + i] = entries
+    // of row i with column < (b << csr_bshift) (rows sorted by column, <= 255 entries).  0: off.
+    int32_t csr_nblk, csr_bshift;
+    const uint8_t *csr_split;
     // per-shift arrays [nz]
     const cplx *z;
     cplx *pibuf;         // [3][nz] rotating pi_n^k

@@ -99,6 +99,11 @@ cudaError_t launch_tiled_c(int L, const SpmvArgs &a, const KParams &kp, double J
 cudaError_t launch_tiled_d(int L, const SpmvArgs &a, const KParams &kp, double J, int grid, cudaStream_t s);
 cudaError_t launch_csr(const SpmvArgs &a, const KParams &kp, const int64_t *row_ptr, const int32_t *col,
                        const void *val, bool cplx_val, double avg_nnz, cudaStream_t s);
+// Column-blocked CSR passes (spmv.cu): split points + qualification statistics, block size, switch.
+cudaError_t launch_csr_split(int64_t M, const int64_t *rp, const int32_t *col, int nblk, int bshift,
+                             uint8_t *split, unsigned long long *stats, cudaStream_t s);
+int csr_block_shift();
+int csr_blocked_env();   // -1: automatic, 0: off, 1: forced where the rows qualify
 // Reverse communication: a.q holds the caller's q = H r.
 cudaError_t launch_rc_dot(const SpmvArgs &a, const KParams &kp, cudaStream_t s);
 

@@ -284,6 +284,145 @@ csr_row_kernel(SpmvArgs a, KParams kp, const int64_t *__restrict__ rp, const int
     spmv_exit(a, kp, agent, w, sc);
 }
 
+// Column-blocked variant of csr_row_kernel (kp.csr_nblk passes, one launch each):
+// pass b applies the entries whose column lies in block b = [b << bshift, (b + 1) << bshift), so
+// the gathers of one pass fall into a slice of r that stays in L2 (a random 16-B gather from a
+// vector larger than L2 costs ~100-128 B of DRAM traffic each).  MODE 0: first pass (q written),
+// 1: middle (q accumulated), 2: last (q accumulated, w partials, CTA 0 = finish agent).
+template <bool CV, int NRHS, int MODE>
+__global__ void __launch_bounds__(kThreads)
+csr_block_kernel(SpmvArgs a, KParams kp, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                 const void *__restrict__ valv, int b) {
+    __shared__ StepScratch sc;
+    bool agent = false;
+    int buf = 0;
+    if (MODE == 2) {
+        if (!spmv_enter(a, agent, buf, sc, kp)) return;
+    } else {
+        pdl_wait();
+        if (a.st) {   // (the finish of the previous iteration runs in the last pass: a terminal
+                      // state decided there leaves the earlier passes' work unused)
+            if (a.st->status != ST_ITERATING) return;
+            buf = (int)(a.st->seq % 3);
+        }
+    }
+    const cplx *__restrict__ r = pick3(a.r, buf);
+    const cplx *__restrict__ t = pick3(a.t, buf);
+    const uint8_t *__restrict__ s0p = kp.csr_split + (int64_t)b * a.M, *__restrict__ s1p = s0p + a.M;
+    const int off = (MODE == 2 && a.st) ? 1 : 0;
+    cplx w = mk(0.0, 0.0);
+    if (!agent) {
+        for (int64_t i = (int64_t)(blockIdx.x - off) * blockDim.x + threadIdx.x; i < a.M;
+             i += (int64_t)(gridDim.x - off) * blockDim.x) {
+            const int64_t e00 = rp[i];
+            const int64_t e0 = e00 + s0p[i], e1 = e00 + s1p[i];
+            cplx acc = mk(0.0, 0.0), acct = mk(0.0, 0.0);
+            if (MODE != 0) {
+                acc = a.q[i];
+                if (NRHS == 2) acct = a.qt[i];
+            }
+            for (int64_t e = e0; e < e1; e += 4) {
+                int c[4];
+                cplx v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool in = e + u < e1;
+                    c[u] = in ? col[e + u] : -1;
+                    if (CV) v[u] = in ? ((const cplx *)valv)[e + u] : mk(0, 0);
+                    else v[u] = mk(in ? ((const double *)valv)[e + u] : 0.0, 0.0);
+                }
+                cplx x[4], xt[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    x[u] = c[u] >= 0 ? r[c[u]] : mk(0, 0);
+                    if (NRHS == 2) xt[u] = c[u] >= 0 ? t[c[u]] : mk(0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (CV) {
+                        acc = cfma(v[u], x[u], acc);
+                        if (NRHS == 2) acct = cfma(v[u], xt[u], acct);
+                    } else {
+                        acc.x = fma(v[u].x, x[u].x, acc.x);
+                        acc.y = fma(v[u].x, x[u].y, acc.y);
+                        if (NRHS == 2) { acct.x = fma(v[u].x, xt[u].x, acct.x); acct.y = fma(v[u].x, xt[u].y, acct.y); }
+                    }
+                }
+            }
+            a.q[i] = acc;
+            if (NRHS == 2) a.qt[i] = acct;
+            if (MODE == 2) w = NRHS == 2 ? cfma_conj(t[i], acc, w) : cfma(r[i], acc, w);
+        }
+    }
+    if (MODE == 2) spmv_exit(a, kp, agent, w, sc);
+}
+
+// Per-row split points of the column blocks (see KParams::csr_split) and what decides whether
+// blocking applies: stats[0] |= 1 when a row is longer than 255 entries or not sorted by column;
+// stats[1] += entries whose column is at least half a block away from the row (the far gathers).
+__global__ void csr_split_kernel(int64_t M, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                 int nblk, int bshift, uint8_t *split, unsigned long long *stats) {
+    unsigned long long far = 0;
+    bool bad = false;
+    const int64_t half = (int64_t(1) << bshift) >> 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e0 = rp[i], e1 = rp[i + 1];
+        if (e1 - e0 > 255) { bad = true; continue; }
+        int bnext = 0, prev = -1;   // split[b][i] for b < bnext is written
+        for (int64_t e = e0; e < e1; ++e) {
+            const int c = col[e];
+            bad |= c < prev;
+            prev = c;
+            const int cb = c >> bshift;
+            for (; bnext <= cb && bnext <= nblk; ++bnext) split[(int64_t)bnext * M + i] = (uint8_t)(e - e0);
+            const int64_t d = c > i ? c - i : i - c;
+            far += d >= half;
+        }
+        for (; bnext <= nblk; ++bnext) split[(int64_t)bnext * M + i] = (uint8_t)(e1 - e0);
+    }
+    if (bad) atomicOr(stats, 1ull);
+    if (far) atomicAdd(stats + 1, far);
+}
+
+cudaError_t launch_csr_split(int64_t M, const int64_t *rp, const int32_t *col, int nblk, int bshift,
+                             uint8_t *split, unsigned long long *stats, cudaStream_t s) {
+    csr_split_kernel<<<8 * sm_count(), kThreads, 0, s>>>(M, rp, col, nblk, bshift, split, stats);
+    return cudaGetLastError();
+}
+
+// Column blocks of 2^bshift rows (SHIFTK_CSR_BSHIFT; default 22 = 64 MiB of r per block, half of
+// L2).  SHIFTK_CSR_BLOCKED=0 disables blocking, =1 forces it wherever the rows qualify.
+int csr_block_shift() {
+    static int b = -1;
+    if (b < 0) {
+        const char *e = getenv("SHIFTK_CSR_BSHIFT");
+        b = e ? atoi(e) : 22;
+        if (b < 4) b = 4;
+        if (b > 30) b = 30;
+    }
+    return b;
+}
+int csr_blocked_env() {
+    static int m = -2;
+    if (m == -2) {
+        const char *e = getenv("SHIFTK_CSR_BLOCKED");
+        m = !e ? -1 : (e[0] == '0' ? 0 : 1);
+    }
+    return m;
+}
+
+template <bool CV, int NRHS>
+static cudaError_t launch_csr_blocked_t(const SpmvArgs &a, const KParams &kp, const int64_t *rp, const int32_t *col,
+                                        const void *val, cudaStream_t s) {
+    const int g = csr_blocks(a.M);
+    cudaError_t e = launch_k(csr_block_kernel<CV, NRHS, 0>, g, kThreads, 0, s, true, a, kp, rp, col, val, 0);
+    for (int b = 1; e == cudaSuccess && b + 1 < kp.csr_nblk; ++b)
+        e = launch_k(csr_block_kernel<CV, NRHS, 1>, g, kThreads, 0, s, true, a, kp, rp, col, val, b);
+    if (e == cudaSuccess)
+        e = launch_k(csr_block_kernel<CV, NRHS, 2>, g + 1, kThreads, 0, s, true, a, kp, rp, col, val, kp.csr_nblk - 1);
+    return e;
+}
+
 template <int LPR>
 static void csr_dispatch(const SpmvArgs &a, const KParams &kp, const int64_t *rp, const int32_t *col,
                          const void *val, bool cv, int grid, cudaStream_t s) {
@@ -314,6 +453,12 @@ int csr_blocks(int64_t M) {
 cudaError_t launch_csr(const SpmvArgs &a, const KParams &kp, const int64_t *rp, const int32_t *col,
                        const void *val, bool cv, double avg_nnz, cudaStream_t s) {
     const int grid = csr_blocks(a.M) + (a.st ? 1 : 0);
+    if (kp.csr_nblk >= 2 && a.st && kp.world <= 1) {   // solver mode, column-blocked passes
+        if (cv) return a.bicg ? launch_csr_blocked_t<true, 2>(a, kp, rp, col, val, s)
+                              : launch_csr_blocked_t<true, 1>(a, kp, rp, col, val, s);
+        return a.bicg ? launch_csr_blocked_t<false, 2>(a, kp, rp, col, val, s)
+                      : launch_csr_blocked_t<false, 1>(a, kp, rp, col, val, s);
+    }
     if (csr_mode() == 1) {
         if (cv) {
             const bool p = a.st != nullptr;

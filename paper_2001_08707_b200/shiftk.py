@@ -77,7 +77,8 @@ class sk_info(ctypes.Structure):
     _fields_ = [("split_ahi", ctypes.c_int32), ("spmv_ctas", ctypes.c_int32),
                 ("update_ctas", ctypes.c_int32), ("shift_agents", ctypes.c_int32),
                 ("arena_bytes", ctypes.c_int64), ("split_fuse", ctypes.c_int32),
-                ("left_real", ctypes.c_int32)]
+                ("left_real", ctypes.c_int32), ("csr_col_blocks", ctypes.c_int32),
+                ("csr_block_shift", ctypes.c_int32)]
 
 
 class sk_profile(ctypes.Structure):
@@ -421,7 +422,8 @@ class Solver:
         _check(load().sk_get_info(self._h, ctypes.byref(i)), "sk_get_info")
         return dict(split_ahi=i.split_ahi, spmv_ctas=i.spmv_ctas, update_ctas=i.update_ctas,
                     shift_agents=i.shift_agents, arena_bytes=i.arena_bytes,
-                    split_fuse=i.split_fuse, left_real=i.left_real)
+                    split_fuse=i.split_fuse, left_real=i.left_real,
+                    csr_col_blocks=i.csr_col_blocks, csr_block_shift=i.csr_block_shift)
 
     def debug_timestamps(self) -> np.ndarray:
         out = np.zeros(16, dtype=np.int64)

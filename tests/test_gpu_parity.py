@@ -419,6 +419,34 @@ def test_bond_split_fuse_and_real_left_switches(mode):
     _subprocess(SPLIT_MODES, env)
 
 
+CSR_BLOCKED = """
+import os
+import numpy as np, oracle, synth
+from paper_2001_08707_b200.device import make_solver, to_device
+from test_gpu_parity import run_window
+kind = os.environ["CSR_KIND"]
+p = synth.make_problem("c3", M=1 << 13, nz=16) if kind == "c3" else synth.make_problem("c4", W=64, nz=8, n_left=3)
+g, o, wr, wy = run_window(p, 25, full_check=(kind == "c3"))
+i = g.info()
+assert i["csr_col_blocks"] == int(os.environ["WANT_BLOCKS"]), i
+h = make_solver(to_device(p))   # graph-captured == stepwise, bit for bit
+h.run(g.iterations, poll_every=g.iterations)
+assert np.array_equal(g.residuals(), h.residuals()) and np.array_equal(g.projections(), h.projections())
+assert h.profile()["launches"] >= g.iterations * (1 + i["csr_col_blocks"])
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("kind,bshift,blocks", [("c3", 11, 4), ("c3", 12, 2), ("c4", 10, 4)])
+def test_csr_column_blocked_passes(kind, bshift, blocks):
+    """The column-blocked CSR SpMV (chosen at full-size C3, forced here with
+    SHIFTK_CSR_BLOCKED=1 and small blocks): q accumulated over 2 or 4 passes of 2^bshift
+    columns each, w and the finish agent in the last — oracle windows on scaled C3 (real CSR,
+    COCG, full x) and C4 (complex CSR, two right-hand sides, BiCG), graph == stepwise bitwise."""
+    _subprocess(CSR_BLOCKED, {"SHIFTK_CSR_BLOCKED": "1", "SHIFTK_CSR_BSHIFT": str(bshift),
+                              "CSR_KIND": kind, "WANT_BLOCKS": str(blocks)})
+
+
 def test_tile_pairs_window_and_determinism():
     """L=24 with the bond split off (SHIFTK_HEIS_SPLIT=0): the streaming SpMV works on tile pairs
     across the top spin bit (each the other's periodic partner); oracle window and bit-identical
