@@ -277,9 +277,9 @@ int sk_get_profile(sk_ctx *ctx, sk_profile *out, int32_t reset);
    split_fuse: with the split, the SpMV also folds the r_{n-1} term of EQ-CG-RN-3REC into
    its output, u = H_A r_n - (gamma sr_prev / sr_cur) r_{n-1}, so the update reads u and r_n only.
    left_real: with the split and Im a = 0, the update reads Re a (8 B/row, its own row order).
-   csr_col_blocks: chosen at sk_init for a CSR operator whose vector is well beyond L2 when the
-   rows are sorted by column, at most 255 entries long, and a quarter or more of the entries lie
-   at least half a block from the diagonal (SHIFTK_CSR_BLOCKED=0/1 disables / forces it). */
+   csr_col_blocks: opt-in (environment SHIFTK_CSR_BLOCKED=1; measured slower than one pass on the
+   C3 workload, so off by default) for a one-GPU CSR operator whose rows are sorted by column and
+   at most 255 entries long. */
 typedef struct {
     int32_t split_ahi;       /* see above                                                      */
     int32_t spmv_ctas;       /* worker CTAs (= w partials) of the SpMV                         */

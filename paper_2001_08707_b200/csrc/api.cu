@@ -410,14 +410,14 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         // the fused r_{n-1} term lives in the tiled H_A kernel only
         kp.split_fuse = sk::split_fuse_enabled() && !sk::heis_stream(H->L, M, kp.bicg, true);
     }
-    // column-blocked CSR passes (spmv.cu): a candidate when the vector is well beyond L2 (or when
-    // forced); the split kernel below decides from the rows themselves
+    // column-blocked CSR passes (spmv.cu): opt-in (SHIFTK_CSR_BLOCKED=1) — measured slower than
+    // the one-pass kernel at C3 (4 blocks 4.21 ms, 2 blocks 3.70 ms vs 3.63 ms);
+    // the split kernel below still checks that the rows qualify
     int csr_cand_nblk = 0;
-    if ((H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) && world == 1 && sk::csr_blocked_env() != 0) {
+    if ((H->kind == SK_OP_CSR_REAL || H->kind == SK_OP_CSR_CPLX) && world == 1 && sk::csr_blocked_env() == 1) {
         const int bs = sk::csr_block_shift();
         const int64_t nb = (M + (int64_t(1) << bs) - 1) >> bs;
-        const bool big = (size_t)M * sizeof(cplx) >= (size_t(96) << 20);
-        if (nb >= 2 && nb <= 16 && M < (int64_t(1) << 31) && (big || sk::csr_blocked_env() == 1)) csr_cand_nblk = (int)nb;
+        if (nb >= 2 && nb <= 16 && M < (int64_t(1) << 31)) csr_cand_nblk = (int)nb;
     }
     kp.n_agents = sk::shift_agents(c->nz);
     kp.world = world;
@@ -572,7 +572,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
         if (cudaStreamSynchronize(c->stream)) return bail(fail(SK_ECUDA, "sync"));
     }
     if (csr_cand_nblk) {   // split points of the column blocks; blocking applies when the rows are
-                           // sorted, short, and enough gathers are far (or it is forced)
+                           // sorted and short
         unsigned long long st2[2] = {1, 0};
         const int bs = sk::csr_block_shift();
         if (sk::launch_csr_split(M, H->row_ptr, H->col, csr_cand_nblk, bs, const_cast<uint8_t *>(kp.csr_split),
@@ -580,8 +580,7 @@ int sk_init(sk_ctx **out, const sk_operator *H, const sk_params *p, const sk_dis
             cudaMemcpyAsync(st2, csr_stats, sizeof(st2), cudaMemcpyDeviceToHost, c->stream) ||
             cudaStreamSynchronize(c->stream))
             return bail(fail(SK_ECUDA, "csr split kernel"));
-        const bool far = (double)st2[1] >= 0.25 * (double)H->nnz;
-        if (st2[0] == 0 && (far || sk::csr_blocked_env() == 1)) {
+        if (st2[0] == 0) {
             kp.csr_nblk = csr_cand_nblk;
             kp.csr_bshift = bs;
         }

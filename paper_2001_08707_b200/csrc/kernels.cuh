@@ -63,6 +63,9 @@ inline __host__ __device__ int64_t stream_partials(int64_t ntiles) {
     return ntiles <= kStreamDirect ? ntiles : ntiles + (ntiles + kStreamGroup - 1) / kStreamGroup;
 }
 constexpr int kTileBits = 10;          // Heisenberg tile: 2^10 states per CTA
+#ifndef TILED_SPLIT_MINB
+#define TILED_SPLIT_MINB 4   // resident CTAs per SM of the bond-split tiled kernel (register cap and grid)
+#endif
 
 int stream_blocks(int64_t M);
 // worker CTAs (= partials) of the Heisenberg SpMV; split: the SpMV of a bond-split solver (H_A)

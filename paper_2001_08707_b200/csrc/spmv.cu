@@ -84,7 +84,7 @@ int heisenberg_blocks(int L, int64_t M, int bicg, bool split) {
         // one resident wave (4 CTAs per SM, one slot for the finish agent), tiles grid-strided:
         // no second-wave launches and prologues (measured at C2: 41.1 -> 41.0 us flushed step,
         // 30.7 -> 29.3 us per graph iteration)
-        const int64_t cap = 4 * (int64_t)sm_count() - 1;
+        const int64_t cap = (split ? TILED_SPLIT_MINB : 4) * (int64_t)sm_count() - 1;
         return (int)(ntiles < cap ? ntiles : cap);
     }
     return stream_blocks(M);
@@ -391,7 +391,7 @@ cudaError_t launch_csr_split(int64_t M, const int64_t *rp, const int32_t *col, i
 }
 
 // Column blocks of 2^bshift rows (SHIFTK_CSR_BSHIFT; default 22 = 64 MiB of r per block, half of
-// L2).  SHIFTK_CSR_BLOCKED=0 disables blocking, =1 forces it wherever the rows qualify.
+// L2).  SHIFTK_CSR_BLOCKED=1 enables blocking wherever the rows qualify (default: one pass).
 int csr_block_shift() {
     static int b = -1;
     if (b < 0) {

@@ -22,9 +22,6 @@ namespace sk {
 #ifndef TILED_SPLIT_QCS
 #define TILED_SPLIT_QCS 1
 #endif
-#ifndef TILED_SPLIT_MINB
-#define TILED_SPLIT_MINB 4   // resident CTAs per SM the SPLIT kernel is compiled for (register cap)
-#endif
 
 // Worker CTAs of the fused SPLIT kernel, once per launch (CTA-uniform; ends with a barrier): wait
 // until CTA 0 has published the final state (kp.kflag), then -kappa = -gamma sr_prev / sr_cur
