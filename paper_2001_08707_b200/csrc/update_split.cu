@@ -29,6 +29,11 @@ namespace sk {
 constexpr int kSplitHB = 8;      // spins AHI..L-1 in a B-tile
 constexpr int kSplitTB = 12;     // 2^12 states per B-tile (64 KB per buffer, two buffers)
 constexpr int kSplitNT = 512;    // threads per CTA (one CTA per SM)
+// SPLIT_UPD_RK = 1: the w_B pass takes the thread's own r_{n+1} rows from registers instead of
+// re-reading them from shared memory (one LDS.128 per row less).
+#ifndef SPLIT_UPD_RK
+#define SPLIT_UPD_RK 1
+#endif
 
 static __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
         }
         cp_async_wait<0>();   // this tile's r_n has landed (staged during the previous w_B pass)
         __syncthreads();      // ... for every thread; and W of the previous tile is consumed
+        cplx rk[SPLIT_UPD_RK ? PER : 1];   // the thread's own r_{n+1} rows, kept for the w_B pass
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int e = tid | (k << NB);
@@ -198,6 +204,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
             if (!FUSE) rn = cfma(a_prev, rp[FUSE ? 0 : k], rn);
             rn_[rt + k * kstep] = rn;
             W[e] = rn;
+            if (SPLIT_UPD_RK) rk[SPLIT_UPD_RK ? k : 0] = rn;
             rho = cfma(rn, rn, rho);
             nu.x = fma(rn.x, rn.x, fma(rn.y, rn.y, nu.x));
             if (LRE) g = mk(fma(lr[LRE ? k : 0], rn.x, g.x), fma(lr[LRE ? k : 0], rn.y, g.y));
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(NT, 1) update_split_kernel(KParams kp, const c
                     h.y += p.y;
                 }
             }
-            wbp = cfma(W[e], h, wbp);
+            wbp = cfma(SPLIT_UPD_RK ? rk[SPLIT_UPD_RK ? k : 0] : W[e], h, wbp);
         }
     }
     // CTA partials: rho, ||r||^2, a^dag r (part_u) and w_B (the next half of part_w)
