@@ -324,6 +324,12 @@ typedef int (*sk_allreduce_fn)(void *user, const double *send, double *recv, int
 int sk_ipc_handle(sk_ctx *ctx, void *out64);
 /* A fresh ncclUniqueId (128 bytes); call on one rank and broadcast. */
 int sk_nccl_unique_id(void *out128);
+/* Self-test of the NCCL plumbing on one device (diagnostics; "MPI optional"):
+   a ONE-rank communicator is created on `device` and n doubles (HOST in) are all-reduced with the
+   call the iteration uses (ncclDouble, ncclSum, a user stream) — directly into out1 and, replayed
+   from a captured CUDA graph, into out2 (both HOST [n]; with one rank each equals in).  Returns
+   SK_ENCCL if libnccl cannot be loaded or a NCCL call fails. */
+int sk_nccl_selftest(int32_t device, int64_t n, const double *in_host, double *out1_host, double *out2_host);
 /* Map every other rank's arena (handles: [world][64] from sk_ipc_handle, in rank order), join
    the NCCL communicator and finish the initialisation (global rho_0, ||b||, P b).  Collective. */
 int sk_connect(sk_ctx *ctx, const void *handles, const void *nccl_id);

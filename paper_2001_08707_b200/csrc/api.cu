@@ -749,6 +749,57 @@ int sk_nccl_unique_id(void *out128) {
     return SK_OK;
 }
 
+// One-rank communicator on `device`: the dlopen'ed NCCL entry points, ncclCommInitRank, and the
+// all-reduce the iteration uses (ncclDouble / ncclSum on a user stream) — once directly and once
+// replayed from a captured CUDA graph (sk_run captures the iteration).  out1 / out2 receive the
+// two results (with one rank: the input).
+int sk_nccl_selftest(int32_t device, int64_t n, const double *in_host, double *out1_host, double *out2_host) {
+    if (n < 1 || !in_host || !out1_host || !out2_host) return fail(SK_EINVAL, "null argument / n < 1");
+    if (!nccl().ok) return fail(SK_ENCCL, "libnccl.so.2 not loadable");
+    CK(cudaSetDevice(device));
+    ncclUniqueId id;
+    NK(nccl().getUniqueId(&id));
+    ncclComm_t comm = nullptr;
+    NK(nccl().commInitRank(&comm, 1, id, 0));
+    cudaStream_t s = nullptr;
+    double *d = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    int rc = SK_OK;
+    auto step = [&](cudaError_t e, const char *what) {
+        if (rc == SK_OK && e != cudaSuccess) rc = fail(SK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    auto nstep = [&](ncclResult_t e, const char *what) {
+        if (rc == SK_OK && e != ncclSuccess) rc = fail(SK_ENCCL, std::string(what) + ": " + nccl().getErrorString(e));
+    };
+    step(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    step(cudaMalloc(&d, 3 * sizeof(double) * n), "malloc");
+    if (rc == SK_OK) {
+        step(cudaMemcpyAsync(d, in_host, sizeof(double) * n, cudaMemcpyHostToDevice, s), "h2d");
+        nstep(nccl().allReduce(d, d + n, (size_t)n, ncclDouble, ncclSum, comm, s), "ncclAllReduce");
+        step(cudaStreamSynchronize(s), "sync");
+    }
+    if (rc == SK_OK) {
+        step(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+        nstep(nccl().allReduce(d, d + 2 * n, (size_t)n, ncclDouble, ncclSum, comm, s), "ncclAllReduce (captured)");
+        const cudaError_t e = cudaStreamEndCapture(s, &g);
+        step(e, "end capture");
+        if (rc == SK_OK) step(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+        if (rc == SK_OK) step(cudaGraphLaunch(ge, s), "graph launch");
+        if (rc == SK_OK) step(cudaStreamSynchronize(s), "sync");
+    }
+    if (rc == SK_OK) {
+        step(cudaMemcpy(out1_host, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost), "d2h");
+        step(cudaMemcpy(out2_host, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost), "d2h");
+    }
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (d) cudaFree(d);
+    if (s) cudaStreamDestroy(s);
+    nccl().commDestroy(comm);
+    return rc;
+}
+
 static int map_peers(sk_ctx *c, const void *handles) {
     CK(cudaSetDevice(c->device));
     std::vector<char *> bases(c->world);

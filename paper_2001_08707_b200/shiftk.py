@@ -32,7 +32,7 @@ EXPORTS = ["sk_init", "sk_update", "sk_update_rc", "sk_get_seed_vectors", "sk_ru
            "sk_profile_enable", "sk_get_profile", "sk_copy_solution", "sk_debug_timestamps",
            "sk_ipc_handle", "sk_nccl_unique_id", "sk_connect", "sk_group_create", "sk_group_connect",
            "sk_group_update", "sk_group_run", "sk_group_destroy", "sk_recalc", "sk_checkpoint",
-           "sk_restore", "sk_combine", "sk_gram", "sk_get_info", "sk_connect_host"]
+           "sk_restore", "sk_combine", "sk_gram", "sk_get_info", "sk_connect_host", "sk_nccl_selftest"]
 
 
 class ShiftkError(RuntimeError):
@@ -124,6 +124,7 @@ def load(path: str = LIB_PATH):
         "sk_debug_timestamps": [VP, VP],
         "sk_ipc_handle": [VP, VP],
         "sk_nccl_unique_id": [VP],
+        "sk_nccl_selftest": [I32, I64, VP, VP, VP],
         "sk_connect": [VP, VP, VP],
         "sk_group_create": [P(VP), I32, I32],
         "sk_group_connect": [VP],
@@ -264,6 +265,15 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_char * 128)()
     _check(load().sk_nccl_unique_id(buf), "sk_nccl_unique_id")
     return bytes(buf)
+
+
+def nccl_selftest(x: np.ndarray, device: int = 0):
+    """sk_nccl_selftest: all-reduce ``x`` (float64) over a one-rank communicator, directly and
+    from a captured graph; returns both results."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    o1, o2 = np.empty_like(x), np.empty_like(x)
+    _check(load().sk_nccl_selftest(device, x.size, x.ctypes.data, o1.ctypes.data, o2.ctypes.data), "sk_nccl_selftest")
+    return o1, o2
 
 
 class Solver:

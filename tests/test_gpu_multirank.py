@@ -112,3 +112,14 @@ def test_loopback_group_with_the_streaming_kernel():
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
+
+
+def test_nccl_plumbing_one_rank_communicator():
+    """The NCCL glue of the multi-rank mode (dlopen'ed entry points, ncclCommInitRank, the
+    iteration's ncclDouble / ncclSum all-reduce on a user stream, directly and replayed from a
+    captured graph) on real hardware: with ONE rank the sum is the input, bit for bit.  (Several
+    NCCL ranks need several GPUs; the sharded data plane is covered by the loopback group above and
+    by test_gpu_ipc_two_process.)"""
+    x = np.random.default_rng(11).standard_normal(2 * (2 + 32))   # C4's update dots: 2 + N_left complex
+    o1, o2 = shiftk.nccl_selftest(x)
+    assert np.array_equal(o1, x) and np.array_equal(o2, x)
