@@ -22,11 +22,6 @@ namespace sk {
 #ifndef TILED_SPLIT_QCS
 #define TILED_SPLIT_QCS 1
 #endif
-// TILED_SPLIT_PCG = 1: the SPLIT kernel's whole-tile partner loads use ld.global.cg (no L1
-// allocation: a partner tile is read once per tile).
-#ifndef TILED_SPLIT_PCG
-#define TILED_SPLIT_PCG 0
-#endif
 
 // Worker CTAs of the fused SPLIT kernel, once per launch (CTA-uniform; ends with a barrier): wait
 // until CTA 0 has published the final state (kp.kflag), then -kappa = -gamma sr_prev / sr_cur
@@ -169,7 +164,7 @@ heisenberg_tiled_kernel(SpmvArgs a, KParams kp, double J) {
                 for (int m = 0; m < NB; ++m)
 #pragma unroll
                     for (int k = 0; k < PER; ++k) {
-                        v[m][k] = (SPLIT && TILED_SPLIT_PCG) ? ldcg(pt[m] + k * kThreads) : pt[m][k * kThreads];
+                        v[m][k] = pt[m][k * kThreads];
                         if (NRHS == 2) vt[m][k] = ptt[m][k * kThreads];
                     }
 #pragma unroll
